@@ -1,0 +1,299 @@
+/*
+ * pgl_b200.h — C-ABI of the B200-native PG-SGD layout hot path.
+ *
+ * This is the drop-in boundary between the reference's C++ layout API
+ * (namespace pglayout, /root/reference/proj/include/pglayout/engine.hpp and
+ * metrics.hpp) and libpgl_b200.so (sm_100a CUDA kernels + C++ host driver).
+ * No C++ or torch type crosses it: plain structs, pointers and sizes only.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj):
+ *   pgl_layout_run              <- pglayout::run_layout        include/pglayout/engine.hpp:80-82, src/engine.cpp:323-326
+ *                                  pglayout::run_layout_reuse  include/pglayout/engine.hpp:86-88, src/engine.cpp:328-334
+ *   pgl_sampled_path_stress     <- pglayout::sampled_path_stress include/pglayout/metrics.hpp:49-51, src/metrics.cpp:108-159
+ *   pgl_graph_create/_layout/.. <- same two calls, split so the packed graph stays resident in HBM
+ *                                  across calls (the reference rebuilds nothing either: PangenomeGraph
+ *                                  is immutable, graph.hpp:61-88)
+ *   pgl_make_schedule           <- pglayout::make_schedule     include/pglayout/engine.hpp:44, src/engine.cpp:266-274
+ *   pgl_init_layout             <- pglayout::init_layout       include/pglayout/layout.hpp:91, src/layout.cpp:20-34
+ *   pgl_last_error/_type        <- the typed exceptions of include/pglayout/errors.hpp:10-42
+ *
+ * Error convention: every function returns a pgl_status equal to the
+ * reference ErrorKind + 1 (usage -> 1, input -> 2, internal -> 3; the CLI's
+ * exit codes, tools/pglayout_main.cpp:34-41), plus PGL_E_CALLBACK when the
+ * caller's iteration callback asked to abort. pgl_last_error() gives the
+ * message (thread-local, "TypeName: detail" exactly like errors.hpp:22-27) and
+ * pgl_last_error_type() the concrete exception class so a C++ facade can
+ * rethrow the identical type.
+ *
+ * Threading: calls on different devices from different host threads are
+ * independent (one CUDA stream per call/graph). This is the multi-GPU
+ * scheduler's contract: independent chromosome graphs, no collective.
+ */
+#ifndef PGL_B200_H
+#define PGL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGL_ABI_VERSION 1
+
+/* ---- status / error types ---------------------------------------------- */
+
+typedef enum pgl_status {
+    PGL_OK = 0,
+    PGL_E_USAGE = 1,    /* ErrorKind::usage    (errors.hpp:12) */
+    PGL_E_INPUT = 2,    /* ErrorKind::input */
+    PGL_E_INTERNAL = 3, /* ErrorKind::internal, also every CUDA failure */
+    PGL_E_CALLBACK = 4  /* the iteration callback returned nonzero */
+} pgl_status;
+
+/* One value per exception class of errors.hpp:31-44, same order. */
+typedef enum pgl_error_type {
+    PGL_ERR_NONE = 0,
+    PGL_ERR_INVALID_PARAMETER = 1,
+    PGL_ERR_UNKNOWN_NODE = 2,
+    PGL_ERR_EMPTY_PATH = 3,
+    PGL_ERR_INDEX_OUT_OF_RANGE = 4,
+    PGL_ERR_EMPTY_GRAPH = 5,
+    PGL_ERR_DEGENERATE_GRAPH = 6,
+    PGL_ERR_MALFORMED_LINE = 7,
+    PGL_ERR_UNKNOWN_SEGMENT = 8,
+    PGL_ERR_NO_PATHS = 9,
+    PGL_ERR_NON_FINITE_COORDINATE = 10,
+    PGL_ERR_MALFORMED_ROW = 11,
+    PGL_ERR_COUNT_MISMATCH = 12,
+    PGL_ERR_ZERO_REFERENCE = 13,
+    PGL_ERR_CORPUS_TOO_LARGE = 14,
+    PGL_ERR_CUDA = 100,
+    PGL_ERR_CALLBACK = 101
+} pgl_error_type;
+
+const char* pgl_last_error(void);
+int pgl_last_error_type(void);
+int pgl_abi_version(void);
+/* Number of visible CUDA devices (0 when no GPU / no driver). Never fails. */
+int pgl_device_count(void);
+
+/* ---- configuration ------------------------------------------------------ */
+
+/* Field-for-field LayoutConfig (engine.hpp:13-23), same order and defaults.
+ * Layout-identical to the C++ struct on LP64 (size 56). */
+typedef struct pgl_layout_config {
+    uint64_t global_seed;    /* 42 */
+    uint32_t n_iters;        /* 30 */
+    uint32_t threads;        /* 1; validated >= 1, ignored by the GPU kernel */
+    uint32_t batch_size;     /* 32: steps sharing one cooling decision */
+    uint32_t _pad0;
+    double zipf_theta;       /* 0.99 */
+    uint64_t zipf_space_max; /* 1000 */
+    double eta_min_eps;      /* 0.01 */
+    uint32_t drf;            /* 1, 2 or 4 */
+    uint32_t srf;            /* >= 1 */
+} pgl_layout_config;
+
+void pgl_layout_config_default(pgl_layout_config* cfg);
+
+/* Execution modes of the device engine. */
+typedef enum pgl_mode {
+    /* Hogwild PG-SGD over a persistent grid: every warp is one reference
+     * worker, lanes run consecutive steps of the warp's share, cooling is
+     * decided per batch and is warp-uniform for batch_size % 32 == 0. */
+    PGL_MODE_HOGWILD = 0,
+    /* One device lane replays the reference's threads=1 run exactly: stream
+     * seed_worker(seed, 0), the draw order of engine.cpp:103-172, FP64
+     * coordinates. Bit-identical to pglayout::run_layout(threads=1). */
+    PGL_MODE_REPLAY = 1
+} pgl_mode;
+
+typedef enum pgl_coord_precision {
+    PGL_COORD_F32 = 0, /* one float4 {sx,sy,ex,ey} per node (16 B)   */
+    PGL_COORD_F64 = 1  /* two double2 per node (32 B = one sector)  */
+} pgl_coord_precision;
+
+/* B200-specific knobs kept out of pgl_layout_config so that struct stays
+ * ABI-identical to LayoutConfig. Zero-initialise and set struct_size. */
+typedef struct pgl_layout_ext {
+    uint32_t struct_size;     /* sizeof(pgl_layout_ext) */
+    uint32_t mode;            /* pgl_mode */
+    uint32_t coord_precision; /* pgl_coord_precision */
+    uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
+    uint32_t block_threads;   /* 0 = default (256) */
+    uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
+    uint32_t steps_per_thread_ilp; /* reserved, 0 */
+    uint32_t _reserved[9];
+} pgl_layout_ext;
+
+void pgl_layout_ext_default(pgl_layout_ext* ext);
+
+/* ---- graph view (host memory, borrowed) --------------------------------- */
+
+/* Layout-identical to pglayout::PathStep (graph.hpp:35-41): 24 bytes,
+ * offset @0, node_id @8, seq_len @12, orient @16 (0 = forward, 1 = reverse). */
+typedef struct pgl_path_step {
+    uint64_t offset;
+    uint32_t node_id;
+    uint32_t seq_len;
+    uint8_t orient;
+    uint8_t _pad[7];
+} pgl_path_step;
+
+/* A borrowed view of a built PangenomeGraph (graph.hpp:61-88). The facade
+ * fills path_steps[k] = g.paths[k].steps.data() — zero copy. */
+typedef struct pgl_graph_view {
+    uint64_t n_nodes;
+    const uint64_t* node_len;               /* [n_nodes] NodeRecord::seq_len */
+    uint32_t n_paths;
+    uint32_t _pad0;
+    const pgl_path_step* const* path_steps; /* [n_paths] */
+    const uint64_t* path_n_steps;           /* [n_paths] Path::steps.size() */
+    const uint64_t* path_total_len;         /* [n_paths] Path::total_len */
+} pgl_graph_view;
+
+/* RunStats (engine.hpp:61-70), same field order. */
+typedef struct pgl_run_stats {
+    uint64_t primary_steps;
+    uint64_t updates_attempted;
+    uint64_t updates_applied;
+    uint64_t updates_skipped;
+    uint64_t batches_first_half;
+    uint64_t batches_first_half_cooling;
+    uint64_t batches_second_half;
+    uint64_t batches_second_half_cooling;
+} pgl_run_stats;
+
+/* StressReport (metrics.hpp:13-20), same field order. */
+typedef struct pgl_stress_report {
+    double mean;
+    uint64_t n;
+    double std_dev;
+    double ci_low;
+    double ci_high;
+    uint64_t skipped;
+} pgl_stress_report;
+
+/* IterationCallback (engine.hpp:72-74). `coords` is [4*n_nodes] doubles in
+ * Layout::snapshot order (sx,sy,ex,ey per node, layout.hpp:58-68) when the
+ * caller asked for them, else NULL. Valid only during the call. Return 0 to
+ * continue; nonzero aborts the run with PGL_E_CALLBACK. */
+typedef int (*pgl_iteration_cb)(uint32_t iter, const double* coords, double eta,
+                                double seconds, void* user);
+
+/* ---- one-shot layout: the drop-in for run_layout / run_layout_reuse ----- */
+
+/* reuse = 0: run_layout semantics; reuse = 1: run_layout_reuse (drf in {2,4}).
+ * out_coords: [4*n_nodes] doubles (snapshot order). stats may be NULL. ext may be NULL. */
+int pgl_layout_run(int device, const pgl_graph_view* graph,
+                   const pgl_layout_config* cfg, const pgl_layout_ext* ext,
+                   int reuse, pgl_iteration_cb cb, int cb_wants_coords,
+                   void* user, double* out_coords, pgl_run_stats* stats);
+
+/* ---- resident graph session ---------------------------------------------- */
+
+typedef struct pgl_graph pgl_graph;
+
+typedef struct pgl_graph_info {
+    uint64_t n_nodes;
+    uint32_t n_paths;
+    uint32_t device;
+    uint64_t total_steps;
+    uint64_t total_nucleotides;
+    uint64_t max_path_len;       /* d_max of make_schedule, engine.cpp:269-270 */
+    uint64_t device_bytes;       /* HBM held by the packed graph + layout */
+    uint32_t usable;             /* some path has >= 2 steps (engine.cpp:30-34) */
+    uint32_t _pad0;
+} pgl_graph_info;
+
+/* Pack the graph (step records, cum_steps, guide table) and upload it. */
+int pgl_graph_create(int device, const pgl_graph_view* graph, pgl_graph** out);
+int pgl_graph_destroy(pgl_graph* g);
+int pgl_graph_info_get(const pgl_graph* g, pgl_graph_info* out);
+
+/* Same semantics as pgl_layout_run on an already-resident graph. The final
+ * layout also stays resident on the device (for pgl_graph_stress).
+ * out_coords may be NULL (no device-to-host copy). */
+int pgl_graph_layout(pgl_graph* g, const pgl_layout_config* cfg,
+                     const pgl_layout_ext* ext, int reuse, pgl_iteration_cb cb,
+                     int cb_wants_coords, void* user, double* out_coords,
+                     pgl_run_stats* stats);
+
+/* Device timing of the last pgl_graph_layout: CUDA events on the launching
+ * stream around the SGD kernels only, summed over iterations. */
+typedef struct pgl_timing {
+    double kernel_ms;      /* sum over SGD launches */
+    double init_ms;        /* host init_layout + upload of the initial layout */
+    double total_ms;       /* whole call, host wall */
+    uint32_t launches;     /* SGD kernel launches (one per iteration) */
+    uint32_t grid_blocks;
+    uint32_t block_threads;
+    uint32_t _pad0;
+    uint64_t device_threads; /* resident lanes = concurrent Hogwild workers*32 */
+} pgl_timing;
+
+int pgl_graph_last_timing(const pgl_graph* g, pgl_timing* out);
+
+/* ---- sampled path stress: the drop-in for sampled_path_stress ----------- */
+
+typedef enum pgl_sps_method {
+    /* Counter-based per-sample streams, deterministic fixed-order two-pass
+     * reduction; same estimator as metrics.cpp:108-159, different draws. */
+    PGL_SPS_COUNTER = 0,
+    /* The reference's own per-path xoshiro stream seed_worker(seed, 2^61+pi)
+     * replayed in parallel (jump-ahead + phase scan): the same terms as the
+     * reference, so n and skipped are identical and mean/sd agree to ~1e-15. */
+    PGL_SPS_STREAM = 1
+} pgl_sps_method;
+
+/* coords: host [4*n_nodes] doubles in snapshot order. */
+int pgl_sampled_path_stress(int device, const pgl_graph_view* graph,
+                            const double* coords, uint64_t seed,
+                            uint32_t samples_per_node, uint32_t method,
+                            pgl_stress_report* out);
+
+/* On a resident graph. coords NULL = the layout left on the device by the
+ * last pgl_graph_layout (no host round trip). */
+int pgl_graph_stress(pgl_graph* g, const double* coords, uint64_t seed,
+                     uint32_t samples_per_node, uint32_t method,
+                     pgl_stress_report* out, double* kernel_ms);
+
+/* ---- host-side helpers of the path (bit-exact with the reference) -------- */
+
+/* etas[n_iters] of make_schedule (engine.cpp:251-274). */
+int pgl_make_schedule(const pgl_graph_view* graph, const pgl_layout_config* cfg,
+                      double* etas);
+/* init_layout (layout.cpp:20-34) into out[4*n_nodes]. */
+int pgl_init_layout(const pgl_graph_view* graph, uint64_t seed, double* out);
+
+/* ---- multi-GPU shard scheduler ------------------------------------------ */
+
+/* Lays out n_graphs independent graphs on n_devices GPUs: longest-processing-
+ * time-first assignment by sum|p| * n_iters, one host thread + stream per
+ * device, no collective. out_coords[k] receives graph k's layout (may be
+ * NULL to skip the copy); seconds[k] the per-graph wall time; assignment[k]
+ * the device index used. */
+int pgl_layout_shards(int n_devices, const int* devices, int n_graphs,
+                      const pgl_graph_view* const* graphs,
+                      const pgl_layout_config* cfgs, const pgl_layout_ext* ext,
+                      double* const* out_coords, pgl_run_stats* stats,
+                      double* seconds, int* assignment);
+
+/* ---- synthetic input fixture (host only) --------------------------------- */
+
+/* generate_synthetic_pangenome (synthetic.cpp:24-120): same nodes, walks,
+ * offsets for the same arguments. Edges are not materialised (the layout
+ * path never reads them); n_edges reports their count when requested. */
+typedef struct pgl_synthetic pgl_synthetic;
+int pgl_synthetic_generate(uint64_t seed, uint64_t backbone_nodes,
+                           uint32_t n_paths, double variant_rate,
+                           pgl_synthetic** out);
+int pgl_synthetic_view(const pgl_synthetic* s, pgl_graph_view* view);
+int pgl_synthetic_free(pgl_synthetic* s);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PGL_B200_H */
