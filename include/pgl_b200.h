@@ -212,6 +212,13 @@ int pgl_graph_create(int device, const pgl_graph_view* graph, pgl_graph** out);
 int pgl_graph_destroy(pgl_graph* g);
 int pgl_graph_info_get(const pgl_graph* g, pgl_graph_info* out);
 
+/* Parity hook: copy the packed device index back to the host, decoded.
+ * positions[2*S] = path_position(start), path_position(end) of every step
+ * in path order (graph.hpp:98-109); nodes[S] = PathStep::node_id;
+ * cum[P+1] = cum_steps (graph.hpp:75-76). Any pointer may be NULL. */
+int pgl_graph_export_index(const pgl_graph* g, uint64_t* positions,
+                           uint32_t* nodes, uint64_t* cum);
+
 /* Same semantics as pgl_layout_run on an already-resident graph. The final
  * layout also stays resident on the device (for pgl_graph_stress).
  * out_coords may be NULL (no device-to-host copy). */

@@ -1,0 +1,244 @@
+// pgl_device.cuh — device building blocks of the PG-SGD step on sm_100a.
+//
+// Every function restates one piece of the reference hot loop and keeps its
+// exact arithmetic: the translation unit is compiled with -fmad=false so no
+// double expression is contracted into an FMA, matching the reference's
+// default x86-64 (no-FMA) build bit for bit.
+#pragma once
+
+#include <cstdint>
+
+#include "pgl_internal.hpp"
+
+namespace pgl {
+
+constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
+
+// ---- xoshiro256+ held in registers (rng.hpp:21-47) ------------------------
+
+struct Xo {
+    uint64_t a, b, c, d;
+
+    __device__ __forceinline__ uint64_t next() {
+        const uint64_t out = a + d;
+        const uint64_t t = b << 17;
+        c ^= a;
+        d ^= b;
+        b ^= c;
+        a ^= d;
+        c ^= t;
+        d = (d << 45) | (d >> 19);
+        return out;
+    }
+    // next_uniform: 53 high bits scaled by 2^-53 (rng.hpp:35-37)
+    __device__ __forceinline__ double uniform() {
+        return static_cast<double>(next() >> 11) * 0x1.0p-53;
+    }
+    // flip_coin: top bit (rng.hpp:40)
+    __device__ __forceinline__ bool coin() { return (next() >> 63) != 0; }
+    // next_below: high word of the 128-bit product (rng.hpp:44-47)
+    __device__ __forceinline__ uint64_t below(uint64_t n) { return __umul64hi(next(), n); }
+};
+
+__host__ __device__ __forceinline__ uint64_t splitmix_next(uint64_t& st) {
+    uint64_t z = (st += kPhi);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// seed_worker (rng.hpp:63-71): GPU lane t draws the reference worker-t stream.
+__host__ __device__ __forceinline__ void seed_worker(uint64_t seed, uint64_t worker, uint64_t s[4]) {
+    uint64_t key = seed ^ (kPhi * (worker + 1));
+    for (int w = 0; w < 4; ++w) s[w] = splitmix_next(key);
+    if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = kPhi;
+}
+
+// ---- Zipf by rejection inversion (rng.hpp:103-144) ------------------------
+
+__device__ __forceinline__ double zipf_helper1(double x) {
+    if (fabs(x) > 1e-8) return log1p(x) / x;
+    return 1.0 - x * (0.5 - x * (1.0 / 3.0 - 0.25 * x));
+}
+__device__ __forceinline__ double zipf_helper2(double x) {
+    if (fabs(x) > 1e-8) return expm1(x) / x;
+    return 1.0 + x * 0.5 * (1.0 + x * (1.0 / 3.0) * (1.0 + 0.25 * x));
+}
+__device__ __forceinline__ double zipf_H(double theta, double x) {
+    const double lx = log(x);
+    return zipf_helper2((1.0 - theta) * lx) * lx;
+}
+__device__ __forceinline__ double zipf_h(double theta, double x) { return exp(-theta * log(x)); }
+__device__ __forceinline__ double zipf_Hinv(double theta, double x) {
+    double t = x * (1.0 - theta);
+    if (t < -1.0) t = -1.0;
+    return exp(zipf_helper1(t) * x);
+}
+
+__device__ __forceinline__ uint64_t zipf_sample(const PathConst& pc, double theta, Xo& r) {
+    if (pc.zn == 1) return 1;
+    for (;;) {
+        const double u = pc.hxn + r.uniform() * (pc.hx1 - pc.hxn);
+        const double x = zipf_Hinv(theta, u);
+        uint64_t k = static_cast<uint64_t>(x + 0.5);
+        if (k < 1)
+            k = 1;
+        else if (k > pc.zn)
+            k = pc.zn;
+        const double kd = static_cast<double>(k);
+        if (kd - x <= pc.s || u >= zipf_H(theta, kd + 0.5) - zipf_h(theta, kd)) return k;
+    }
+}
+
+// ---- graph index reads ------------------------------------------------------
+
+__device__ __forceinline__ StepRec load_step(const StepRec* p) {
+    // Read-only, random, no reuse: non-coherent path, skip L1 allocation.
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return StepRec{v.x, v.y, v.z, v.w};
+}
+
+// path_position (graph.hpp:98-109): `end` selects Endpoint::end.
+__device__ __forceinline__ uint64_t step_pos(const StepRec& r, int end) {
+    return end ? (static_cast<uint64_t>(r.pe_lo) | (static_cast<uint64_t>(r.hi >> 16) << 32))
+               : (static_cast<uint64_t>(r.ps_lo) | (static_cast<uint64_t>(r.hi & 0xFFFFu) << 32));
+}
+
+// weighted_step_select (graph.hpp:123-138): the reference binary-searches
+// cum_steps; a guide table indexed by the draw's top bits lands on the
+// answer's path or just before it, so the search becomes 1-2 compares.
+__device__ __forceinline__ uint32_t select_path(const DevGraph& g, uint64_t x, uint64_t pick) {
+    uint32_t p = __ldg(g.guide + (x >> (64 - g.guide_bits)));
+    while (__ldg(g.cum + p + 1) <= pick) ++p;
+    return p;
+}
+
+// ---- coordinate store ---------------------------------------------------------
+// F32: one float4 {sx,sy,ex,ey} per node (16 B). F64: two double2 per node
+// (32 B, one sector). Hogwild contract (layout.hpp:12-15): an
+// endpoint is read and written as one 8/16-byte access (no torn scalar),
+// through L2 (.cg) so a lane never re-reads a stale L1 line.
+
+template <typename T> struct Coord;
+
+template <> struct Coord<float> {
+    __device__ __forceinline__ static void get(const void* base, uint32_t node, int end,
+                                               double& x, double& y) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(base) + 2 * static_cast<uint64_t>(node) + end);
+        x = static_cast<double>(v.x);
+        y = static_cast<double>(v.y);
+    }
+    __device__ __forceinline__ static void set(void* base, uint32_t node, int end, double x, double y) {
+        __stcg(reinterpret_cast<float2*>(base) + 2 * static_cast<uint64_t>(node) + end,
+               make_float2(static_cast<float>(x), static_cast<float>(y)));
+    }
+};
+
+template <> struct Coord<double> {
+    __device__ __forceinline__ static void get(const void* base, uint32_t node, int end,
+                                               double& x, double& y) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(base) + 2 * static_cast<uint64_t>(node) + end);
+        x = v.x;
+        y = v.y;
+    }
+    __device__ __forceinline__ static void set(void* base, uint32_t node, int end, double x, double y) {
+        __stcg(reinterpret_cast<double2*>(base) + 2 * static_cast<uint64_t>(node) + end, make_double2(x, y));
+    }
+};
+
+// apply_endpoint_update (engine.cpp:276-306). Both endpoints are read before
+// either is written and i is stored before j, so an aliased pair (a path
+// revisiting a node) resolves exactly as the reference: j's value wins.
+template <typename T>
+__device__ __forceinline__ bool apply_update(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                             double d_ref, double eta, Xo& r) {
+    if (!(d_ref > 0.0)) return false;
+    const double w = 1.0 / (d_ref * d_ref);
+    double mu = eta * w;
+    if (mu > 1.0) mu = 1.0;
+    double vix, viy, vjx, vjy;
+    Coord<T>::get(coords, ni, ei, vix, viy);
+    Coord<T>::get(coords, nj, ej, vjx, vjy);
+    const double dx = vix - vjx;
+    const double dy = viy - vjy;
+    const double mag = sqrt(dx * dx + dy * dy);
+    double ux, uy;
+    if (mag < 1e-9) {
+        const double angle = 2.0 * 3.14159265358979323846 * r.uniform();
+        ux = cos(angle);
+        uy = sin(angle);
+    } else {
+        ux = dx / mag;
+        uy = dy / mag;
+    }
+    const double delta = mu * (mag - d_ref) / 2.0;
+    Coord<T>::set(coords, ni, ei, vix - delta * ux, viy - delta * uy);
+    Coord<T>::set(coords, nj, ej, vjx + delta * ux, vjy + delta * uy);
+    return true;
+}
+
+__device__ __forceinline__ double abs_diff(uint64_t a, uint64_t b) {
+    return static_cast<double>(a > b ? a - b : b - a);
+}
+
+// One full step after the batch decision: select_step_pair (engine.cpp:52-80),
+// the endpoint coins (:137-138), the update (:139-145) and the drf>1 extra
+// combinations (:147-170). Returns the number of applied updates; the
+// caller counts drf - applied as skipped.
+template <typename T>
+__device__ __forceinline__ uint32_t pgsgd_step(const DevGraph& g, void* coords, Xo& r,
+                                               bool cooling, double eta, double theta,
+                                               uint32_t drf) {
+    const uint64_t x = r.next();
+    const uint64_t pick = __umul64hi(x, g.total_steps);
+    const uint32_t p = select_path(g, x, pick);
+    const PathConst pc = g.pc[p];
+    const int64_t n = static_cast<int64_t>(pc.n);
+    if (n < 2) return 0;
+    const int64_t i = static_cast<int64_t>(pick - pc.base);
+    int64_t j;
+    if (cooling) {
+        const int64_t k = static_cast<int64_t>(zipf_sample(pc, theta, r));
+        const int64_t sign = r.coin() ? 1 : -1;
+        j = i + sign * k;
+        if (j < 0 || j >= n) {
+            j = i - sign * k;
+            if (j < 0 || j >= n) {
+                j = i + sign * k;
+                j = j < 0 ? 0 : (j > n - 1 ? n - 1 : j);
+            }
+        }
+        if (j == i) return 0;
+    } else {
+        j = static_cast<int64_t>(r.below(pc.n));
+        if (j == i) {
+            j = static_cast<int64_t>(r.below(pc.n));
+            if (j == i) return 0;
+        }
+    }
+    const StepRec ri = load_step(g.step + pc.base + i);
+    const StepRec rj = load_step(g.step + pc.base + j);
+    const int ei = r.coin() ? 0 : 1;  // coin true -> Endpoint::start (engine.cpp:89-91)
+    const int ej = r.coin() ? 0 : 1;
+    uint32_t applied = apply_update<T>(coords, ri.node, ei, rj.node, ej,
+                                       abs_diff(step_pos(ri, ei), step_pos(rj, ej)), eta, r);
+    if (drf > 1) {
+        unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+        for (uint32_t extra = 1; extra < drf; ++extra) {
+            int a, b;
+            do {
+                a = r.coin() ? 0 : 1;
+                b = r.coin() ? 0 : 1;
+            } while (used & (1u << ((a ? 2 : 0) | (b ? 1 : 0))));
+            used |= 1u << ((a ? 2 : 0) | (b ? 1 : 0));
+            applied += apply_update<T>(coords, ri.node, a, rj.node, b,
+                                       abs_diff(step_pos(ri, a), step_pos(rj, b)), eta, r);
+        }
+    }
+    return applied;
+}
+
+}  // namespace pgl

@@ -1,0 +1,988 @@
+// pgl_host.cpp — host driver and C-ABI of libpgl_b200.so.
+//
+// Host side of the drop-in for pglayout::run_layout / run_layout_reuse /
+// sampled_path_stress (engine.cpp:174-247, metrics.cpp:108-159):
+//   validate_config (engine.cpp:15-28) -> make_schedule (:251-274) ->
+//   init_layout (layout.cpp:20-34, bit-exact, FP64) -> pack the graph into
+//   16-byte step records + guide table -> H2D -> n_iters kernel launches on
+//   one stream -> D2H of the coordinates in Layout::snapshot order.
+// Everything here is plain C++ (g++, -ffp-contract=off); the device code is
+// in pgl_sgd.cu / pgl_sps.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "pgl_internal.hpp"
+
+namespace pgl {
+
+namespace {
+
+const char* const kTypeNames[] = {
+    "",           "InvalidParameter", "UnknownNode",   "EmptyPath",      "IndexOutOfRange",
+    "EmptyGraph", "DegenerateGraph",  "MalformedLine", "UnknownSegment", "NoPaths",
+    "NonFiniteCoordinate", "MalformedRow", "CountMismatch", "ZeroReference", "CorpusTooLarge"};
+
+// ErrorKind of each exception class (errors.hpp:31-44) -> status.
+int status_of(int type) {
+    switch (type) {
+        case PGL_ERR_INVALID_PARAMETER: return PGL_E_USAGE;
+        case PGL_ERR_INDEX_OUT_OF_RANGE: return PGL_E_INTERNAL;
+        case PGL_ERR_CUDA: return PGL_E_INTERNAL;
+        case PGL_ERR_CALLBACK: return PGL_E_CALLBACK;
+        case PGL_ERR_NONE: return PGL_OK;
+        default: return type <= PGL_ERR_CORPUS_TOO_LARGE ? PGL_E_INPUT : PGL_E_INTERNAL;
+    }
+}
+
+thread_local std::string t_err;
+thread_local int t_err_type = 0;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        t_err.clear();
+        t_err_type = 0;
+        return PGL_OK;
+    } catch (const Failure& f) {
+        t_err = f.what();
+        t_err_type = f.type;
+        return status_of(f.type);
+    } catch (const std::bad_alloc&) {
+        t_err = "host allocation failed";
+        t_err_type = PGL_ERR_CUDA;
+        return PGL_E_INTERNAL;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        t_err_type = PGL_ERR_CUDA;
+        return PGL_E_INTERNAL;
+    }
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+unsigned host_threads() {
+    const unsigned h = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(h ? h : 1u, 64u));
+}
+
+template <typename F>
+void parallel_for(uint64_t n, F&& f) {  // f(begin, end)
+    const unsigned T = static_cast<unsigned>(std::min<uint64_t>(host_threads(), std::max<uint64_t>(1, n / 65536)));
+    if (T <= 1) {
+        f(uint64_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+        pool.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T); });
+    for (auto& th : pool) th.join();
+}
+
+// ---- reference host math, restated --------------------------------------
+
+constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
+
+struct HostRng {  // xoshiro256+ (rng.hpp:13-48)
+    uint64_t s[4];
+    HostRng(uint64_t seed, uint64_t worker) {
+        uint64_t key = seed ^ (kPhi * (worker + 1));
+        for (auto& w : s) {
+            uint64_t z = (key += kPhi);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            w = z ^ (z >> 31);
+        }
+        if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = kPhi;
+    }
+    uint64_t next() {
+        const uint64_t out = s[0] + s[3], t = s[1] << 17;
+        s[2] ^= s[0];
+        s[3] ^= s[1];
+        s[1] ^= s[2];
+        s[0] ^= s[3];
+        s[2] ^= t;
+        s[3] = (s[3] << 45) | (s[3] >> 19);
+        return out;
+    }
+    double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    bool coin() { return (next() >> 63) != 0; }
+    uint64_t below(uint64_t n) { return static_cast<uint64_t>((static_cast<unsigned __int128>(next()) * n) >> 64); }
+};
+
+constexpr uint64_t kStreamInit = 1ULL << 62;   // rng.hpp:76
+constexpr uint64_t kStreamSynth = 1ULL << 60;  // rng.hpp:78
+
+void validate_config(const pgl_layout_config& c) {  // engine.cpp:15-28
+    if (c.n_iters < 1) raise(PGL_ERR_INVALID_PARAMETER, "n_iters must be >= 1");
+    if (c.threads < 1) raise(PGL_ERR_INVALID_PARAMETER, "threads must be >= 1");
+    if (c.batch_size < 1) raise(PGL_ERR_INVALID_PARAMETER, "batch_size must be >= 1");
+    if (!(c.zipf_theta > 0.0) || !std::isfinite(c.zipf_theta))
+        raise(PGL_ERR_INVALID_PARAMETER, "zipf_theta must be positive");
+    if (c.zipf_space_max < 1) raise(PGL_ERR_INVALID_PARAMETER, "zipf_space_max must be >= 1");
+    if (!(c.eta_min_eps > 0.0)) raise(PGL_ERR_INVALID_PARAMETER, "eta_min_eps must be positive");
+    if (c.drf != 1 && c.drf != 2 && c.drf != 4) raise(PGL_ERR_INVALID_PARAMETER, "drf must be 1, 2 or 4");
+    if (c.srf < 1) raise(PGL_ERR_INVALID_PARAMETER, "srf must be >= 1");
+}
+
+void eta_schedule(double eta_max, double eta_min, uint32_t n, double* etas) {  // engine.cpp:251-264
+    if (n < 1) raise(PGL_ERR_INVALID_PARAMETER, "schedule needs n_iters >= 1");
+    if (!(eta_max > 0.0) || !(eta_min > 0.0) || !(eta_min <= eta_max))
+        raise(PGL_ERR_INVALID_PARAMETER, "schedule needs 0 < eta_min <= eta_max");
+    const double lambda = n > 1 ? std::log(eta_max / eta_min) / (n - 1) : 0.0;
+    for (uint32_t t = 0; t < n; ++t) etas[t] = eta_max * std::exp(-lambda * t);
+}
+
+// Summary of a graph view, computed once.
+struct ViewSummary {
+    uint64_t total_steps = 0, total_nt = 0, max_path_len = 0;
+    bool usable = false;
+};
+
+ViewSummary summarize(const pgl_graph_view* v) {
+    if (!v) raise(PGL_ERR_INVALID_PARAMETER, "graph view is null");
+    if (v->n_paths && (!v->path_steps || !v->path_n_steps || !v->path_total_len))
+        raise(PGL_ERR_INVALID_PARAMETER, "graph view has paths but null path arrays");
+    if (v->n_nodes && !v->node_len) raise(PGL_ERR_INVALID_PARAMETER, "graph view has nodes but no node_len");
+    ViewSummary s;
+    for (uint64_t n = 0; n < v->n_nodes; ++n) s.total_nt += v->node_len[n];
+    for (uint32_t p = 0; p < v->n_paths; ++p) {
+        if (v->path_n_steps[p] == 0) raise(PGL_ERR_EMPTY_PATH, "path " + std::to_string(p) + " has no steps");
+        s.total_steps += v->path_n_steps[p];
+        s.max_path_len = std::max(s.max_path_len, v->path_total_len[p]);
+        if (v->path_n_steps[p] >= 2) s.usable = true;
+    }
+    return s;
+}
+
+void schedule_for(const pgl_graph_view* v, const ViewSummary& s, const pgl_layout_config& c, double* etas) {
+    if (v->n_paths == 0 || !s.usable) raise(PGL_ERR_DEGENERATE_GRAPH, "schedule needs a path pair with d_ref > 0");
+    const uint64_t dmax = std::max<uint64_t>(1, s.max_path_len);  // engine.cpp:269-270
+    eta_schedule(static_cast<double>(dmax) * static_cast<double>(dmax), c.eta_min_eps, c.n_iters, etas);
+}
+
+// init_layout (layout.cpp:20-34): x = running offset in node-id order, y
+// uniform in +-sqrt(total nt) from stream seed_worker(seed, 2^62), start
+// then end per node. Sequential by construction (one stream).
+void init_layout(const pgl_graph_view* v, uint64_t total_nt, uint64_t seed, double* out) {
+    HostRng r(seed, kStreamInit);
+    const double amp = std::sqrt(static_cast<double>(total_nt));
+    uint64_t off = 0;
+    for (uint64_t n = 0; n < v->n_nodes; ++n) {
+        out[4 * n + 0] = static_cast<double>(off);
+        out[4 * n + 1] = (2.0 * r.uniform() - 1.0) * amp;
+        out[4 * n + 2] = static_cast<double>(off + v->node_len[n]);
+        out[4 * n + 3] = (2.0 * r.uniform() - 1.0) * amp;
+        off += v->node_len[n];
+    }
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count <= n && p) return;
+        release();
+        PGL_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b) {
+        if (b <= bytes && p) return;
+        release();
+        PGL_CUDA(cudaHostAlloc(&p, b, cudaHostAllocDefault));
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~PinnedBuf() { release(); }
+};
+
+struct DeviceGuard {  // restores the caller's current device
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        PGL_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+[[noreturn]] void raise(int type, const std::string& detail) {
+    const char* name = (type >= 0 && type <= PGL_ERR_CORPUS_TOO_LARGE) ? kTypeNames[type] : "CudaError";
+    throw Failure(type, std::string(name) + ": " + detail);
+}
+
+[[noreturn]] void raise_cuda(int err, const char* what, const char* file, int line) {
+    throw Failure(PGL_ERR_CUDA, std::string("CudaError: ") + cudaGetErrorString(static_cast<cudaError_t>(err)) +
+                                    " in " + what + " (" + file + ":" + std::to_string(line) + ")");
+}
+
+void zipf_constants(uint64_t n, double theta, double* hx1, double* hxn, double* s) {
+    // ZipfSampler ctor (rng.hpp:91-98) with its helpers (:122-144).
+    auto helper1 = [](double x) { return std::abs(x) > 1e-8 ? std::log1p(x) / x : 1.0 - x * (0.5 - x * (1.0 / 3.0 - 0.25 * x)); };
+    auto helper2 = [](double x) {
+        return std::abs(x) > 1e-8 ? std::expm1(x) / x : 1.0 + x * 0.5 * (1.0 + x * (1.0 / 3.0) * (1.0 + 0.25 * x));
+    };
+    auto H = [&](double x) {
+        const double lx = std::log(x);
+        return helper2((1.0 - theta) * lx) * lx;
+    };
+    auto h = [&](double x) { return std::exp(-theta * std::log(x)); };
+    auto Hinv = [&](double x) {
+        double t = x * (1.0 - theta);
+        if (t < -1.0) t = -1.0;
+        return std::exp(helper1(t) * x);
+    };
+    *hx1 = H(1.5) - 1.0;
+    *hxn = H(static_cast<double>(n) + 0.5);
+    *s = 2.0 - Hinv(H(2.5) - h(2.0));
+}
+
+void finish_report(pgl_stress_report* r, double ssd) {  // metrics.cpp:14-23
+    r->std_dev = r->n >= 2 ? std::sqrt(ssd / static_cast<double>(r->n - 1)) : 0.0;
+    const double half = r->n > 0 ? 1.96 * r->std_dev / std::sqrt(static_cast<double>(r->n)) : 0.0;
+    r->ci_low = r->mean - half;
+    r->ci_high = r->mean + half;
+}
+
+}  // namespace pgl
+
+using namespace pgl;
+
+// ---- the resident graph ------------------------------------------------------
+
+struct pgl_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t n_nodes = 0;
+    uint32_t n_paths = 0;
+    ViewSummary sum;
+    std::vector<uint64_t> node_len;      // host copy (init_layout)
+    std::vector<uint64_t> path_n_steps;  // host copy (zipf supports)
+    DevBuf<StepRec> step;
+    DevBuf<uint64_t> cum;
+    DevBuf<uint32_t> guide;
+    DevBuf<PathConst> pc;
+    uint32_t guide_bits = 8;
+    DevBuf<double> coords64;             // [4V] FP64 layout / staging
+    DevBuf<float> coords32;              // [4V] FP32 layout
+    int layout_f64 = -1;                 // precision of the resident layout (-1: none)
+    DevBuf<uint64_t> rng;                // SoA xoshiro states
+    DevBuf<unsigned long long> stats;    // [8]
+    SpsScratch sps{};
+    pgl_timing timing{};
+    PinnedBuf pin;
+
+    ~pgl_graph() {
+        if (sps.part) cudaFree(sps.part);
+        if (sps.cnt) cudaFree(sps.cnt);
+        if (sps.scal) cudaFree(sps.scal);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    DevGraph dev() const {
+        DevGraph d;
+        d.step = step.p;
+        d.cum = cum.p;
+        d.guide = guide.p;
+        d.pc = pc.p;
+        d.total_steps = sum.total_steps;
+        d.n_paths = n_paths;
+        d.guide_bits = guide_bits;
+        d.n_nodes = n_nodes;
+        return d;
+    }
+};
+
+namespace {
+
+// Pack the borrowed reference-format view into 16-byte step records,
+// multithreaded on the host, streamed through two pinned chunks so packing
+// overlaps the H2D copy.
+void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
+    const uint64_t S = G->sum.total_steps;
+    const uint32_t P = v->n_paths;
+    std::vector<uint64_t> cum(P + 1, 0);
+    for (uint32_t p = 0; p < P; ++p) cum[p + 1] = cum[p] + v->path_n_steps[p];
+    for (uint32_t p = 0; p < P; ++p)
+        if (v->path_total_len[p] >= (1ULL << 48))
+            raise(PGL_ERR_INVALID_PARAMETER, "path longer than 2^48 nucleotides");
+
+    G->step.alloc(S);
+    G->cum.alloc(P + 1);
+    PGL_CUDA(cudaMemcpyAsync(G->cum.p, cum.data(), (P + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, G->stream));
+
+    // guide table: bucket b of the top guide_bits of the selection draw
+    // starts at pick floor(b * S / 2^bits); store the path containing it.
+    uint32_t bits = 8;
+    while ((1u << bits) < 8u * std::max<uint32_t>(P, 1) && bits < 16) ++bits;
+    G->guide_bits = bits;
+    std::vector<uint32_t> guide(1u << bits, 0);
+    for (uint64_t b = 0; b < guide.size(); ++b) {
+        const uint64_t first = static_cast<uint64_t>((static_cast<unsigned __int128>(b) * S) >> bits);
+        guide[b] = static_cast<uint32_t>(std::upper_bound(cum.begin(), cum.end(), first) - cum.begin() - 1);
+        if (guide[b] >= P) guide[b] = P ? P - 1 : 0;
+    }
+    G->guide.alloc(guide.size());
+    PGL_CUDA(cudaMemcpyAsync(G->guide.p, guide.data(), guide.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                             G->stream));
+
+    constexpr uint64_t kChunk = 1ULL << 22;  // 4 Mi steps = 64 MiB of records
+    G->pin.alloc(2 * kChunk * sizeof(StepRec));
+    StepRec* bufs[2] = {static_cast<StepRec*>(G->pin.p), static_cast<StepRec*>(G->pin.p) + kChunk};
+    cudaEvent_t done[2];
+    PGL_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    PGL_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    std::atomic<int> bad_node{0};
+    const uint64_t n_chunks = (S + kChunk - 1) / kChunk;
+    for (uint64_t c = 0; c < n_chunks; ++c) {
+        StepRec* buf = bufs[c & 1];
+        if (c >= 2) PGL_CUDA(cudaEventSynchronize(done[c & 1]));
+        const uint64_t k0 = c * kChunk, k1 = std::min(S, k0 + kChunk);
+        parallel_for(k1 - k0, [&](uint64_t b, uint64_t e) {
+            uint64_t k = k0 + b;
+            uint32_t p = static_cast<uint32_t>(std::upper_bound(cum.begin(), cum.end(), k) - cum.begin() - 1);
+            for (; k < k0 + e; ++k) {
+                while (k >= cum[p + 1]) ++p;
+                const pgl_path_step& st = v->path_steps[p][k - cum[p]];
+                if (st.node_id >= v->n_nodes) bad_node.store(1, std::memory_order_relaxed);
+                // path_position (graph.hpp:98-109): the far side of a
+                // forward visit is its end, of a reverse visit its start.
+                const uint64_t near = st.offset, far = st.offset + st.seq_len;
+                const uint64_t ps = st.orient ? far : near, pe = st.orient ? near : far;
+                buf[k - k0] = StepRec{st.node_id, static_cast<uint32_t>(ps), static_cast<uint32_t>(pe),
+                                      static_cast<uint32_t>((ps >> 32) | ((pe >> 32) << 16))};
+            }
+        });
+        PGL_CUDA(cudaMemcpyAsync(G->step.p + k0, buf, (k1 - k0) * sizeof(StepRec), cudaMemcpyHostToDevice,
+                                 G->stream));
+        PGL_CUDA(cudaEventRecord(done[c & 1], G->stream));
+    }
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+    if (bad_node.load()) raise(PGL_ERR_UNKNOWN_NODE, "path references a node outside the graph");
+}
+
+pgl_graph* create_graph(int device, const pgl_graph_view* v) {
+    const ViewSummary s = summarize(v);
+    DeviceGuard dg(device);
+    auto G = std::make_unique<pgl_graph>();
+    G->device = device;
+    PGL_CUDA(cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking));
+    G->n_nodes = v->n_nodes;
+    G->n_paths = v->n_paths;
+    G->sum = s;
+    if (v->n_nodes >= (1ULL << 32)) raise(PGL_ERR_INVALID_PARAMETER, "more than 2^32 nodes");
+    G->node_len.assign(v->node_len, v->node_len + v->n_nodes);
+    G->path_n_steps.assign(v->path_n_steps, v->path_n_steps + v->n_paths);
+    pack_graph(G.get(), v);
+    G->stats.alloc(8);
+    return G.release();
+}
+
+// Resident view-like accessors for the schedule/init helpers.
+pgl_graph_view view_of(const pgl_graph* G) {
+    pgl_graph_view v{};
+    v.n_nodes = G->n_nodes;
+    v.node_len = G->node_len.data();
+    v.n_paths = G->n_paths;
+    return v;
+}
+
+uint32_t auto_max_warps(uint64_t n_nodes) {
+    // Hogwild concurrency cap: keep the number of in-flight updates well
+    // below the number of endpoints so concurrent read-modify-writes on one
+    // endpoint stay rare (SURVEY.md §7 hard part 1). One warp per 64 nodes,
+    // at least 4 warps.
+    const uint64_t w = n_nodes / 64;
+    return static_cast<uint32_t>(std::max<uint64_t>(4, std::min<uint64_t>(w, 1u << 24)));
+}
+
+void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_ext* extp, int reuse,
+                  pgl_iteration_cb cb, int cb_wants_coords, void* user, double* out_coords,
+                  pgl_run_stats* stats_out) {
+    const double t_call = now_s();
+    if (!cfgp) raise(PGL_ERR_INVALID_PARAMETER, "config is null");
+    const pgl_layout_config cfg = *cfgp;
+    pgl_layout_ext ext;
+    pgl_layout_ext_default(&ext);
+    if (extp) {
+        if (extp->struct_size < 16 || extp->struct_size > sizeof(pgl_layout_ext))
+            raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.struct_size mismatch");
+        std::memcpy(&ext, extp, extp->struct_size);
+    }
+    if (reuse) {  // run_layout_reuse, engine.cpp:328-334
+        if (cfg.drf != 2 && cfg.drf != 4) raise(PGL_ERR_INVALID_PARAMETER, "update reuse needs drf of 2 or 4");
+        if (cfg.srf < 1) raise(PGL_ERR_INVALID_PARAMETER, "srf must be >= 1");
+    }
+    validate_config(cfg);
+    if (G->n_paths == 0 || !G->sum.usable)
+        raise(PGL_ERR_DEGENERATE_GRAPH, "layout needs at least one path with two or more steps");
+    if (ext.mode != PGL_MODE_HOGWILD && ext.mode != PGL_MODE_REPLAY) raise(PGL_ERR_INVALID_PARAMETER, "unknown mode");
+    if (ext.coord_precision > 1) raise(PGL_ERR_INVALID_PARAMETER, "unknown coord_precision");
+
+    DeviceGuard dg(G->device);
+    const pgl_graph_view hv = view_of(G);
+    std::vector<double> etas(cfg.n_iters);
+    {  // make_schedule (engine.cpp:266-274): eta_max = (longest path)^2
+        const uint64_t dmax = std::max<uint64_t>(1, G->sum.max_path_len);
+        eta_schedule(static_cast<double>(dmax) * static_cast<double>(dmax), cfg.eta_min_eps, cfg.n_iters,
+                     etas.data());
+    }
+
+    const int replay = ext.mode == PGL_MODE_REPLAY;
+    const int f64 = replay ? 1 : static_cast<int>(ext.coord_precision);
+    const uint64_t V = G->n_nodes;
+
+    // init_layout on the host (bit-exact), upload, narrow to FP32 on device.
+    const double t_init = now_s();
+    G->pin.alloc(std::max<size_t>(G->pin.bytes, 4 * V * sizeof(double)));
+    double* hinit = static_cast<double*>(G->pin.p);
+    init_layout(&hv, G->sum.total_nt, cfg.global_seed, hinit);
+    G->coords64.alloc(4 * V);
+    PGL_CUDA(cudaMemcpyAsync(G->coords64.p, hinit, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+    void* coords = G->coords64.p;
+    if (!f64) {
+        G->coords32.alloc(4 * V);
+        launch_f64_to_f32(G->coords64.p, G->coords32.p, 4 * V, G->stream);
+        coords = G->coords32.p;
+    }
+
+    // per-path constants for this config (zipf_params_for, engine.cpp:36-39)
+    std::vector<PathConst> pcs(G->n_paths);
+    {
+        uint64_t base = 0;
+        std::vector<std::pair<uint64_t, std::array<double, 3>>> memo;
+        for (uint32_t p = 0; p < G->n_paths; ++p) {
+            const uint64_t n = G->path_n_steps[p];
+            const uint64_t span = n < 2 ? 1 : n - 1;
+            const uint64_t zn = std::min<uint64_t>(span, cfg.zipf_space_max);
+            PathConst c{base, n, zn, 0, 0, 0};
+            auto it = std::find_if(memo.begin(), memo.end(), [&](auto& m) { return m.first == zn; });
+            if (it == memo.end()) {
+                std::array<double, 3> k;
+                zipf_constants(zn, cfg.zipf_theta, &k[0], &k[1], &k[2]);
+                memo.emplace_back(zn, k);
+                it = memo.end() - 1;
+            }
+            c.hx1 = it->second[0];
+            c.hxn = it->second[1];
+            c.s = it->second[2];
+            pcs[p] = c;
+            base += n;
+        }
+    }
+    G->pc.alloc(pcs.size());
+    PGL_CUDA(cudaMemcpyAsync(G->pc.p, pcs.data(), pcs.size() * sizeof(PathConst), cudaMemcpyHostToDevice,
+                             G->stream));
+    PGL_CUDA(cudaMemsetAsync(G->stats.p, 0, 8 * sizeof(unsigned long long), G->stream));
+
+    // RNG states: lane t <- seed_worker(seed, t) (rng.hpp:63-71)
+    LaunchShape shape;
+    uint32_t n_warps = 1;
+    uint64_t lanes = 1;
+    if (!replay) {
+        const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
+        shape = sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads));
+        const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
+        n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
+        lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
+    } else {
+        lanes = 1;
+    }
+    G->rng.alloc(4 * std::max<uint64_t>(lanes, 1));
+    DevRng rng{G->rng.p, G->rng.p + lanes, G->rng.p + 2 * lanes, G->rng.p + 3 * lanes};
+    launch_seed_rng(rng, lanes, cfg.global_seed, G->stream);
+
+    // L2 persistence window on the coordinate array (fits: C1/C2 sizes).
+    const size_t coord_bytes = 4 * V * (f64 ? sizeof(double) : sizeof(float));
+    if (ext.l2_persist && !replay) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, G->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, G->device);
+        if (max_persist > 0 && max_window > 0) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(coord_bytes, max_persist));
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = coords;
+            attr.accessPolicyWindow.num_bytes = std::min<size_t>(coord_bytes, max_window);
+            attr.accessPolicyWindow.hitRatio =
+                std::min(1.0f, static_cast<float>(max_persist) / static_cast<float>(std::max<size_t>(coord_bytes, 1)));
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(G->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+        }
+    }
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
+    const double init_ms = (now_s() - t_init) * 1e3;
+
+    const uint64_t spi = 10 * G->sum.total_steps / cfg.srf;  // engine.cpp:197
+    const DevGraph dg_ = G->dev();
+    DevStats* dstats = reinterpret_cast<DevStats*>(G->stats.p);
+    std::vector<cudaEvent_t> ev(2 * cfg.n_iters);
+    for (auto& e : ev) PGL_CUDA(cudaEventCreate(&e));
+    std::vector<double> host_coords;
+    bool aborted = false;
+    for (uint32_t it = 0; it < cfg.n_iters && !aborted; ++it) {
+        const double t_it = now_s();
+        IterArgs a;
+        a.eta = etas[it];
+        a.theta = cfg.zipf_theta;
+        a.steps = spi;
+        a.force_cooling = 2ULL * it >= static_cast<uint64_t>(cfg.n_iters) ? 1 : 0;  // engine.cpp:202-203
+        a.batch = cfg.batch_size;
+        a.drf = cfg.drf;
+        a.n_warps = n_warps;
+        PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
+        if (replay)
+            launch_sgd_replay(dg_, G->coords64.p, G->rng.p, dstats, a, G->stream);
+        else
+            launch_sgd_hogwild(dg_, coords, f64, rng, dstats, a, shape, G->stream);
+        PGL_CUDA(cudaEventRecord(ev[2 * it + 1], G->stream));
+        if (cb) {  // IterationCallback at the boundary (engine.cpp:223-229)
+            const double* cptr = nullptr;
+            if (cb_wants_coords) {
+                host_coords.resize(4 * V);
+                if (!f64) launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+                PGL_CUDA(cudaMemcpyAsync(host_coords.data(), G->coords64.p, 4 * V * sizeof(double),
+                                         cudaMemcpyDeviceToHost, G->stream));
+                cptr = host_coords.data();
+            }
+            PGL_CUDA(cudaStreamSynchronize(G->stream));
+            if (cb(it, cptr, a.eta, now_s() - t_it, user) != 0) aborted = true;
+        }
+    }
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
+    G->layout_f64 = f64;
+    double kms = 0.0;
+    uint32_t launches = 0;
+    for (uint32_t it = 0; it < cfg.n_iters; ++it) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]) == cudaSuccess) {
+            kms += ms;
+            ++launches;
+        }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (aborted) raise(PGL_ERR_CALLBACK, "iteration callback requested abort");
+
+    unsigned long long dst[8];
+    PGL_CUDA(cudaMemcpy(dst, G->stats.p, sizeof dst, cudaMemcpyDeviceToHost));
+    if (stats_out) {
+        pgl_run_stats st{};
+        st.primary_steps = static_cast<uint64_t>(cfg.n_iters) * spi;
+        st.updates_attempted = st.primary_steps * cfg.drf;
+        st.updates_applied = dst[2];
+        st.updates_skipped = st.updates_attempted - dst[2];
+        st.batches_first_half = dst[4];
+        st.batches_first_half_cooling = dst[5];
+        st.batches_second_half = dst[6];
+        st.batches_second_half_cooling = dst[7];
+        *stats_out = st;
+    }
+    if (out_coords) {
+        if (!f64) launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+        PGL_CUDA(cudaMemcpyAsync(out_coords, G->coords64.p, 4 * V * sizeof(double), cudaMemcpyDeviceToHost,
+                                 G->stream));
+        PGL_CUDA(cudaStreamSynchronize(G->stream));
+    }
+    if (ext.l2_persist && !replay) {
+        cudaStreamAttrValue attr{};
+        attr.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(G->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+        cudaCtxResetPersistingL2Cache();
+    }
+    G->timing.kernel_ms = kms;
+    G->timing.launches = launches;
+    G->timing.init_ms = init_ms;
+    G->timing.grid_blocks = replay ? 1 : static_cast<uint32_t>(shape.blocks);
+    G->timing.block_threads = replay ? 1 : static_cast<uint32_t>(shape.threads);
+    G->timing.device_threads = replay ? 1 : static_cast<uint64_t>(n_warps) * 32;
+    G->timing.total_ms = (now_s() - t_call) * 1e3;
+}
+
+void graph_stress(pgl_graph* G, const double* coords, uint64_t seed, uint32_t spn, uint32_t method,
+                  pgl_stress_report* out, double* kernel_ms) {
+    if (spn < 1) raise(PGL_ERR_INVALID_PARAMETER, "samples_per_node must be >= 1");
+    if (!out) raise(PGL_ERR_INVALID_PARAMETER, "report is null");
+    DeviceGuard dg(G->device);
+    const uint64_t V = G->n_nodes;
+    const void* dc;
+    int f64;
+    if (coords) {
+        G->coords64.alloc(4 * V);
+        PGL_CUDA(cudaMemcpyAsync(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+        dc = G->coords64.p;
+        f64 = 1;
+        G->layout_f64 = -1;  // the resident layout is overwritten
+    } else {
+        if (G->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
+        f64 = G->layout_f64;
+        dc = f64 ? static_cast<const void*>(G->coords64.p) : static_cast<const void*>(G->coords32.p);
+    }
+    std::memset(out, 0, sizeof *out);
+    if (method == PGL_SPS_COUNTER)
+        run_sps_counter(G->dev(), dc, f64, seed, spn, G->sps, out, kernel_ms, G->stream);
+    else if (method == PGL_SPS_STREAM)
+        run_sps_stream(G->dev(), dc, f64, seed, spn, out, kernel_ms, G->stream);
+    else
+        raise(PGL_ERR_INVALID_PARAMETER, "unknown sampled stress method");
+}
+
+// ---- synthetic fixture (synthetic.cpp:24-120, walks only) ----------------------
+
+struct Synthetic {
+    std::vector<uint64_t> node_len;
+    std::vector<std::vector<pgl_path_step>> paths;
+    std::vector<const pgl_path_step*> ptrs;
+    std::vector<uint64_t> n_steps, totals;
+};
+
+Synthetic* generate(uint64_t seed, uint64_t B, uint32_t n_paths, double rate) {
+    if (B < 2) raise(PGL_ERR_INVALID_PARAMETER, "backbone needs at least 2 nodes");
+    if (n_paths < 1) raise(PGL_ERR_INVALID_PARAMETER, "need at least one path");
+    if (!(rate >= 0.0 && rate <= 1.0)) raise(PGL_ERR_INVALID_PARAMETER, "variant_rate must lie in [0, 1]");
+    enum : uint8_t { SNV = 0, INS = 1, DEL = 2, NONE = 3 };
+    HostRng r(seed, kStreamSynth);
+    std::vector<uint8_t> bb_len(B), kind(B, NONE), alt_len(B, 0);
+    for (uint64_t b = 0; b < B; ++b) bb_len[b] = static_cast<uint8_t>(8 + r.below(25));
+    for (uint64_t b = 0; b < B; ++b) {
+        if (r.uniform() >= rate) continue;
+        uint8_t feas[3];
+        uint64_t nf = 0;
+        if (b + 3 <= B) feas[nf++] = SNV;
+        if (b + 2 <= B) feas[nf++] = INS;
+        if (b + 3 <= B) feas[nf++] = DEL;
+        if (nf == 0) continue;
+        kind[b] = feas[r.below(nf)];
+        if (kind[b] != DEL) alt_len[b] = static_cast<uint8_t>(8 + r.below(25));
+    }
+    auto S = std::make_unique<Synthetic>();
+    std::vector<uint32_t> bb_id(B), alt_id(B, 0);
+    S->node_len.reserve(B + B / 8);
+    for (uint64_t b = 0; b < B; ++b) {
+        bb_id[b] = static_cast<uint32_t>(S->node_len.size());
+        S->node_len.push_back(bb_len[b]);
+        if (kind[b] == INS) {
+            alt_id[b] = static_cast<uint32_t>(S->node_len.size());
+            S->node_len.push_back(alt_len[b]);
+        }
+        if (b >= 1 && kind[b - 1] == SNV) {
+            alt_id[b - 1] = static_cast<uint32_t>(S->node_len.size());
+            S->node_len.push_back(alt_len[b - 1]);
+        }
+    }
+    if (S->node_len.size() >= (1ULL << 32)) raise(PGL_ERR_INVALID_PARAMETER, "too many nodes");
+    S->paths.resize(n_paths);
+    for (uint32_t p = 0; p < n_paths; ++p) {
+        auto& steps = S->paths[p];
+        steps.reserve(B + B / 16);
+        uint64_t off = 0;
+        auto push = [&](uint32_t id) {
+            const uint32_t len = static_cast<uint32_t>(S->node_len[id]);
+            steps.push_back(pgl_path_step{off, id, len, 0, {}});
+            off += len;
+        };
+        uint64_t b = 0;
+        while (b < B) {
+            push(bb_id[b]);
+            if (kind[b] != NONE && r.coin()) {
+                if (kind[b] == SNV) {
+                    push(alt_id[b]);
+                    b += 2;
+                } else if (kind[b] == INS) {
+                    push(alt_id[b]);
+                    b += 1;
+                } else {
+                    b += 2;
+                }
+                continue;
+            }
+            b += 1;
+        }
+        S->totals.push_back(off);
+        S->n_steps.push_back(steps.size());
+        S->ptrs.push_back(steps.data());
+    }
+    return S.release();
+}
+
+}  // namespace
+
+struct pgl_synthetic : Synthetic {};
+
+// ---- C ABI -----------------------------------------------------------------------
+
+extern "C" {
+
+const char* pgl_last_error(void) { return t_err.c_str(); }
+int pgl_last_error_type(void) { return t_err_type; }
+int pgl_abi_version(void) { return PGL_ABI_VERSION; }
+
+int pgl_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void pgl_layout_config_default(pgl_layout_config* c) {  // engine.hpp:13-23
+    std::memset(c, 0, sizeof *c);
+    c->global_seed = 42;
+    c->n_iters = 30;
+    c->threads = 1;
+    c->batch_size = 32;
+    c->zipf_theta = 0.99;
+    c->zipf_space_max = 1000;
+    c->eta_min_eps = 0.01;
+    c->drf = 1;
+    c->srf = 1;
+}
+
+void pgl_layout_ext_default(pgl_layout_ext* e) {
+    std::memset(e, 0, sizeof *e);
+    e->struct_size = sizeof(pgl_layout_ext);
+    e->mode = PGL_MODE_HOGWILD;
+    e->coord_precision = PGL_COORD_F32;
+}
+
+int pgl_graph_create(int device, const pgl_graph_view* v, pgl_graph** out) {
+    return guarded([&] {
+        if (!out) raise(PGL_ERR_INVALID_PARAMETER, "out is null");
+        *out = create_graph(device, v);
+    });
+}
+
+int pgl_graph_destroy(pgl_graph* g) {
+    return guarded([&] {
+        if (!g) return;
+        DeviceGuard dg(g->device);
+        delete g;
+    });
+}
+
+int pgl_graph_info_get(const pgl_graph* g, pgl_graph_info* out) {
+    return guarded([&] {
+        if (!g || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        std::memset(out, 0, sizeof *out);
+        out->n_nodes = g->n_nodes;
+        out->n_paths = g->n_paths;
+        out->device = static_cast<uint32_t>(g->device);
+        out->total_steps = g->sum.total_steps;
+        out->total_nucleotides = g->sum.total_nt;
+        out->max_path_len = g->sum.max_path_len;
+        out->device_bytes = g->step.n * sizeof(StepRec) + g->cum.n * 8 + g->guide.n * 4 + g->pc.n * sizeof(PathConst) +
+                            g->coords64.n * 8 + g->coords32.n * 4 + g->rng.n * 8;
+        out->usable = g->sum.usable ? 1 : 0;
+    });
+}
+
+int pgl_graph_export_index(const pgl_graph* g, uint64_t* positions, uint32_t* nodes, uint64_t* cum) {
+    return guarded([&] {
+        if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
+        DeviceGuard dg(g->device);
+        const uint64_t S = g->sum.total_steps;
+        std::vector<StepRec> recs(S);
+        if (S) PGL_CUDA(cudaMemcpy(recs.data(), g->step.p, S * sizeof(StepRec), cudaMemcpyDeviceToHost));
+        for (uint64_t k = 0; k < S; ++k) {
+            const StepRec& r = recs[k];
+            if (positions) {
+                positions[2 * k] = static_cast<uint64_t>(r.ps_lo) | (static_cast<uint64_t>(r.hi & 0xFFFFu) << 32);
+                positions[2 * k + 1] = static_cast<uint64_t>(r.pe_lo) | (static_cast<uint64_t>(r.hi >> 16) << 32);
+            }
+            if (nodes) nodes[k] = r.node;
+        }
+        if (cum) PGL_CUDA(cudaMemcpy(cum, g->cum.p, (g->n_paths + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    });
+}
+
+int pgl_graph_layout(pgl_graph* g, const pgl_layout_config* cfg, const pgl_layout_ext* ext, int reuse,
+                     pgl_iteration_cb cb, int cb_wants_coords, void* user, double* out_coords,
+                     pgl_run_stats* stats) {
+    return guarded([&] {
+        if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
+        graph_layout(g, cfg, ext, reuse, cb, cb_wants_coords, user, out_coords, stats);
+    });
+}
+
+int pgl_graph_last_timing(const pgl_graph* g, pgl_timing* out) {
+    return guarded([&] {
+        if (!g || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *out = g->timing;
+    });
+}
+
+int pgl_layout_run(int device, const pgl_graph_view* v, const pgl_layout_config* cfg, const pgl_layout_ext* ext,
+                   int reuse, pgl_iteration_cb cb, int cb_wants_coords, void* user, double* out_coords,
+                   pgl_run_stats* stats) {
+    return guarded([&] {
+        // Validate before touching the device, in the reference's order
+        // (engine.cpp:176-179; reuse checks first, engine.cpp:330-332).
+        if (!cfg) raise(PGL_ERR_INVALID_PARAMETER, "config is null");
+        if (reuse) {
+            if (cfg->drf != 2 && cfg->drf != 4) raise(PGL_ERR_INVALID_PARAMETER, "update reuse needs drf of 2 or 4");
+            if (cfg->srf < 1) raise(PGL_ERR_INVALID_PARAMETER, "srf must be >= 1");
+        }
+        validate_config(*cfg);
+        const ViewSummary s = summarize(v);
+        if (v->n_paths == 0 || !s.usable)
+            raise(PGL_ERR_DEGENERATE_GRAPH, "layout needs at least one path with two or more steps");
+        std::unique_ptr<pgl_graph> G(create_graph(device, v));
+        graph_layout(G.get(), cfg, ext, reuse, cb, cb_wants_coords, user, out_coords, stats);
+        DeviceGuard dg(device);
+        G.reset();
+    });
+}
+
+int pgl_graph_stress(pgl_graph* g, const double* coords, uint64_t seed, uint32_t spn, uint32_t method,
+                     pgl_stress_report* out, double* kernel_ms) {
+    return guarded([&] {
+        if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
+        graph_stress(g, coords, seed, spn, method, out, kernel_ms);
+    });
+}
+
+int pgl_sampled_path_stress(int device, const pgl_graph_view* v, const double* coords, uint64_t seed, uint32_t spn,
+                            uint32_t method, pgl_stress_report* out) {
+    return guarded([&] {
+        if (spn < 1) raise(PGL_ERR_INVALID_PARAMETER, "samples_per_node must be >= 1");
+        if (!coords) raise(PGL_ERR_INVALID_PARAMETER, "coords is null");
+        std::unique_ptr<pgl_graph> G(create_graph(device, v));
+        graph_stress(G.get(), coords, seed, spn, method, out, nullptr);
+        DeviceGuard dg(device);
+        G.reset();
+    });
+}
+
+int pgl_make_schedule(const pgl_graph_view* v, const pgl_layout_config* cfg, double* etas) {
+    return guarded([&] {
+        if (!cfg || !etas) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        const ViewSummary s = summarize(v);
+        schedule_for(v, s, *cfg, etas);
+    });
+}
+
+int pgl_init_layout(const pgl_graph_view* v, uint64_t seed, double* out) {
+    return guarded([&] {
+        if (!v || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        uint64_t nt = 0;
+        for (uint64_t n = 0; n < v->n_nodes; ++n) nt += v->node_len[n];
+        init_layout(v, nt, seed, out);
+    });
+}
+
+int pgl_synthetic_generate(uint64_t seed, uint64_t backbone, uint32_t n_paths, double rate, pgl_synthetic** out) {
+    return guarded([&] {
+        if (!out) raise(PGL_ERR_INVALID_PARAMETER, "out is null");
+        *out = static_cast<pgl_synthetic*>(generate(seed, backbone, n_paths, rate));
+    });
+}
+
+int pgl_synthetic_view(const pgl_synthetic* s, pgl_graph_view* v) {
+    return guarded([&] {
+        if (!s || !v) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        std::memset(v, 0, sizeof *v);
+        v->n_nodes = s->node_len.size();
+        v->node_len = s->node_len.data();
+        v->n_paths = static_cast<uint32_t>(s->paths.size());
+        v->path_steps = s->ptrs.data();
+        v->path_n_steps = s->n_steps.data();
+        v->path_total_len = s->totals.data();
+    });
+}
+
+int pgl_synthetic_free(pgl_synthetic* s) {
+    delete static_cast<Synthetic*>(s);
+    return PGL_OK;
+}
+
+int pgl_layout_shards(int n_devices, const int* devices, int n_graphs, const pgl_graph_view* const* graphs,
+                      const pgl_layout_config* cfgs, const pgl_layout_ext* ext, double* const* out_coords,
+                      pgl_run_stats* stats, double* seconds, int* assignment) {
+    return guarded([&] {
+        if (n_devices < 1 || !devices) raise(PGL_ERR_INVALID_PARAMETER, "need at least one device");
+        if (n_graphs < 0 || (n_graphs && (!graphs || !cfgs))) raise(PGL_ERR_INVALID_PARAMETER, "null graph list");
+        // LPT: heaviest graph first onto the least-loaded device.
+        std::vector<double> work(n_graphs);
+        for (int k = 0; k < n_graphs; ++k) {
+            const ViewSummary s = summarize(graphs[k]);
+            validate_config(cfgs[k]);
+            work[k] = static_cast<double>(s.total_steps) * cfgs[k].n_iters * cfgs[k].drf / cfgs[k].srf;
+        }
+        std::vector<int> order(n_graphs);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
+        std::vector<double> load(n_devices, 0.0);
+        std::vector<std::vector<int>> queue(n_devices);
+        for (int k : order) {
+            const int d = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+            load[d] += work[k];
+            queue[d].push_back(k);
+            if (assignment) assignment[k] = d;
+        }
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(n_devices);
+        std::vector<int> err_types(n_devices, 0);
+        for (int d = 0; d < n_devices; ++d)
+            pool.emplace_back([&, d] {
+                try {
+                    for (int k : queue[d]) {
+                        const double t0 = now_s();
+                        std::unique_ptr<pgl_graph> G(create_graph(devices[d], graphs[k]));
+                        graph_layout(G.get(), &cfgs[k], ext, 0, nullptr, 0, nullptr,
+                                     out_coords ? out_coords[k] : nullptr, stats ? &stats[k] : nullptr);
+                        {
+                            DeviceGuard dg(devices[d]);
+                            G.reset();
+                        }
+                        if (seconds) seconds[k] = now_s() - t0;
+                    }
+                } catch (const Failure& f) {
+                    errs[d] = f.what();
+                    err_types[d] = f.type;
+                } catch (const std::exception& e) {
+                    errs[d] = e.what();
+                    err_types[d] = PGL_ERR_CUDA;
+                }
+            });
+        for (auto& t : pool) t.join();
+        for (int d = 0; d < n_devices; ++d)
+            if (err_types[d]) throw Failure(err_types[d], errs[d]);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// pgl_internal.hpp — declarations shared by the host driver (pgl_host.cpp)
+// and the sm_100a kernels (pgl_sgd.cu, pgl_sps.cu). Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pgl_b200.h"
+
+namespace pgl {
+
+// Typed failure carrying the reference exception class (errors.hpp:31-44).
+struct Failure : std::runtime_error {
+    int type;
+    Failure(int t, const std::string& m) : std::runtime_error(m), type(t) {}
+};
+
+[[noreturn]] void raise(int type, const std::string& detail);
+[[noreturn]] void raise_cuda(int err, const char* what, const char* file, int line);
+
+#define PGL_CUDA(call)                                                         \
+    do {                                                                       \
+        const int pgl_e_ = static_cast<int>(call);                             \
+        if (pgl_e_ != 0) ::pgl::raise_cuda(pgl_e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+// ---- device-side data layout --------
+
+// One path step, 16 bytes = half a 32-byte sector, 16-byte aligned so a
+// random gather touches exactly one sector. The orientation is folded into
+// the two endpoint positions (path_position, graph.hpp:98-109):
+//   x = node id
+//   y = low 32 bits of pos(start endpoint)   z = low 32 bits of pos(end endpoint)
+//   w = (pos_start >> 32) | (pos_end >> 32) << 16     (positions < 2^48)
+struct alignas(16) StepRec {
+    uint32_t node, ps_lo, pe_lo, hi;
+};
+
+// Per-path constants, 48 bytes: step range, Zipf support and the rejection-
+// inversion constants of ZipfSampler (rng.hpp:95-97) computed on the host
+// with the same libm as the reference.
+struct alignas(16) PathConst {
+    uint64_t base;    // cum_steps[p]
+    uint64_t n;       // |p|
+    uint64_t zn;      // Zipf support n = min(max(|p|-1,1), zipf_space_max)
+    double hx1, hxn, s;
+};
+
+// Everything a kernel needs to read the resident graph.
+struct DevGraph {
+    const StepRec* step;      // [S]
+    const uint64_t* cum;      // [P+1]
+    const uint32_t* guide;    // [1 << guide_bits] path of the bucket's first pick
+    const PathConst* pc;      // [P]
+    uint64_t total_steps;
+    uint32_t n_paths;
+    uint32_t guide_bits;
+    uint64_t n_nodes;
+};
+
+struct IterArgs {
+    double eta;
+    double theta;
+    uint64_t steps;       // primary steps this iteration (all warps)
+    uint32_t force_cooling;
+    uint32_t batch;
+    uint32_t drf;
+    uint32_t n_warps;     // Hogwild workers = resident warps
+};
+
+// Device RNG states, structure of arrays (coalesced): s[k][lane].
+struct DevRng {
+    uint64_t* s0;
+    uint64_t* s1;
+    uint64_t* s2;
+    uint64_t* s3;
+};
+
+// Accumulated on device with warp-aggregated atomics; RunStats order.
+struct DevStats {
+    unsigned long long v[8];
+};
+
+// ---- kernel launchers (pgl_sgd.cu / pgl_sps.cu) ---------------------------
+
+struct LaunchShape {
+    int blocks = 0;
+    int threads = 256;
+};
+
+// Occupancy-derived persistent grid for the Hogwild kernel.
+LaunchShape sgd_shape(int device, int coord_f64, uint32_t max_warps, int block_threads);
+
+void launch_seed_rng(DevRng rng, uint64_t n_lanes, uint64_t seed, void* stream);
+void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng rng,
+                        DevStats* stats, const IterArgs& a, LaunchShape shape,
+                        void* stream);
+void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4,
+                       DevStats* stats, const IterArgs& a, void* stream);
+
+struct SpsScratch {
+    double* part;            // [n_chunks]
+    unsigned long long* cnt; // [2]: n, skipped
+    double* scal;            // [4]: sum, mean, ssd, spare
+    uint64_t n_chunks_cap;
+};
+// Counter-based sampled path stress on a resident graph (metrics.cpp:108-159
+// estimator). Fills out (mean, n, sd, ci) deterministically.
+void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64,
+                     uint64_t seed, uint32_t spn, SpsScratch& scratch,
+                     pgl_stress_report* out, double* kernel_ms, void* stream);
+void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64,
+                    uint64_t seed, uint32_t spn, pgl_stress_report* out,
+                    double* kernel_ms, void* stream);
+
+// Small device helpers used by the host driver.
+void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
+void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);
+
+// ---- host helpers (pgl_host.cpp) -----------------------------------------
+
+void zipf_constants(uint64_t n, double theta, double* hx1, double* hxn, double* s);
+void finish_report(pgl_stress_report* r, double sum_sq_dev);
+
+}  // namespace pgl

@@ -1,0 +1,309 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Bars:
+  * index / positions / cum_steps: bit-exact (graph.hpp:98-109, graph.cpp:7-59)
+  * PGL_MODE_REPLAY layouts and RunStats: bit-exact with the reference's
+    threads=1 run (engine.cpp:174-247) restated by the oracle
+  * PGL_SPS_COUNTER: bit-exact with its C restatement, statistically equal to
+    the reference estimator (metrics.cpp:108-159, z-test like
+    test_metrics.cpp:308-327)
+  * Hogwild layouts: RunStats identities exact (test_engine.cpp:257-312),
+    median SPS over seeds 101..105 within 2% of the reference (north star)
+"""
+import numpy as np
+import pytest
+
+from oracle_ffi import make_cfg, stress_tuple
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [(11, 60, 2, 0.1), (3, 50, 4, 0.3), (5, 30, 3, 0.3), (12, 50, 2, 0.1)]
+C1 = (1, 9680, 8, 0.05)
+
+
+def both(pgl, oracle, args):
+    return pgl.generate_synthetic_pangenome(*args), oracle.generate(*args)
+
+
+def cfg_pair(pgl, **kw):
+    return pgl.LayoutConfig(**kw), make_cfg(**kw)
+
+
+def stats_tuple(st):
+    names = ["primary_steps", "updates_attempted", "updates_applied", "updates_skipped",
+             "batches_first_half", "batches_first_half_cooling", "batches_second_half",
+             "batches_second_half_cooling"]
+    return tuple(int(getattr(st, n)) for n in names)
+
+
+def revisit_graph(pgl, oracle):
+    """Reverse steps and node revisits (the aliasing case of engine.cpp:285-304)."""
+    lens = [5, 3, 7, 2, 9, 4]
+    walks = [[(0, 0), (1, 1), (2, 0), (1, 0), (3, 1), (0, 0), (4, 0)],
+             [(5, 1), (2, 1), (2, 1), (3, 0), (4, 1)],
+             [(1, 0)]]
+    return pgl.build_graph(lens, walks), oracle.build(lens, walks)
+
+
+# ---- index -------------------------------------------------------------------------
+
+@pytest.mark.parametrize("args", SMALL + [C1])
+def test_packed_index_bit_exact(pgl, oracle, gpu, args):
+    g, go = both(pgl, oracle, args)
+    fo = oracle.export(go)
+    with pgl.DeviceGraph(g) as dg:
+        pos, nodes, cum = dg.export_index()
+    assert np.array_equal(cum, fo.cum)
+    assert np.array_equal(nodes, fo.step_node)
+    assert np.array_equal(pos, fo.positions())
+
+
+def test_packed_index_reverse_and_revisits(pgl, oracle, gpu):
+    g, go = revisit_graph(pgl, oracle)
+    fo = oracle.export(go)
+    with pgl.DeviceGraph(g) as dg:
+        pos, nodes, cum = dg.export_index()
+    assert np.array_equal(pos, fo.positions())
+    assert np.array_equal(nodes, fo.step_node)
+    assert np.array_equal(cum, fo.cum)
+
+
+# ---- replay mode: bit-exact with the reference's threads=1 run ------------------
+
+REPLAY = [
+    (SMALL[0], dict(n_iters=4, global_seed=77)),
+    (SMALL[1], dict(n_iters=30, global_seed=42)),
+    (SMALL[2], dict(n_iters=3, global_seed=5, batch_size=1)),
+    (SMALL[3], dict(n_iters=3, drf=2, srf=2)),
+    (SMALL[3], dict(n_iters=3, drf=4, srf=4, batch_size=7)),
+    (SMALL[3], dict(n_iters=5, drf=2, srf=1, zipf_space_max=3, zipf_theta=2.0)),
+]
+
+
+@pytest.mark.parametrize("args,kw", REPLAY)
+def test_replay_bit_exact(pgl, oracle, gpu, args, kw):
+    g, go = both(pgl, oracle, args)
+    cfg, ocfg = cfg_pair(pgl, **kw)
+    reuse = kw.get("drf", 1) > 1
+    st = pgl.RunStats()
+    fn = pgl.run_layout_reuse if reuse else pgl.run_layout
+    out = fn(g, cfg, stats=st, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    ref, rst = oracle.run_layout(go, ocfg, reuse=reuse)
+    assert np.array_equal(out, ref), "first diverging coordinate: %s" % np.flatnonzero(out != ref)[:4]
+    assert stats_tuple(st) == stats_tuple(rst)
+
+
+def test_replay_bit_exact_revisits(pgl, oracle, gpu):
+    g, go = revisit_graph(pgl, oracle)
+    cfg, ocfg = cfg_pair(pgl, n_iters=6, global_seed=9, batch_size=3)
+    st = pgl.RunStats()
+    out = pgl.run_layout(g, cfg, stats=st, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    ref, rst = oracle.run_layout(go, ocfg)
+    assert stats_tuple(st) == stats_tuple(rst)
+    # coincident endpoints take the jitter path (cos/sin): allow 1e-9 there
+    np.testing.assert_allclose(out, ref, rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.slow
+def test_replay_bit_exact_config1(pgl, oracle, gpu):
+    g, go = both(pgl, oracle, C1)
+    cfg, ocfg = cfg_pair(pgl, global_seed=101)
+    st = pgl.RunStats()
+    out = pgl.run_layout(g, cfg, stats=st, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    ref, rst = oracle.run_layout(go, ocfg)
+    assert stats_tuple(st) == stats_tuple(rst)
+    assert np.array_equal(out, ref)
+
+
+def test_replay_callback_sees_every_iteration(pgl, oracle, gpu):
+    g, go = both(pgl, oracle, (15, 40, 1, 0.0))
+    cfg, ocfg = cfg_pair(pgl, n_iters=6)
+    seen, ref_seen = [], []
+    pgl.run_layout(g, cfg, on_iteration=lambda it, c, eta, s: seen.append((it, eta, c.copy())),
+                   ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    oracle.run_layout(go, ocfg, callback=lambda it, c, eta: ref_seen.append((it, eta, c)))
+    etas = pgl.make_schedule(g, cfg)
+    assert [s[0] for s in seen] == list(range(6))
+    assert [s[1] for s in seen] == list(etas)
+    for a, b in zip(seen, ref_seen):
+        assert a[0] == b[0] and a[1] == b[1] and np.array_equal(a[2], b[2])
+
+
+# ---- sampled path stress -----------------------------------------------------------
+
+@pytest.mark.parametrize("args,spn", [(SMALL[0], 10), (SMALL[1], 100), (C1, 20), ((2, 80, 2, 0.0), 100)])
+def test_sps_counter_bit_exact(pgl, oracle, gpu, args, spn):
+    g, go = both(pgl, oracle, args)
+    lay, _ = oracle.run_layout(go, make_cfg(n_iters=5))
+    got = pgl.sampled_path_stress(g, lay, 7, spn)
+    want = oracle.sps_counter(go, lay, 7, spn)
+    assert (got.mean, got.n, got.std_dev, got.ci_low, got.ci_high, got.skipped) == stress_tuple(want)
+
+
+def test_sps_counter_on_resident_f32_layout(pgl, oracle, gpu):
+    g, go = both(pgl, oracle, C1)
+    with pgl.DeviceGraph(g) as dg:
+        lay = dg.layout(pgl.LayoutConfig(n_iters=6))
+        got = dg.stress(7, 20)  # reads the float4 layout left on the device
+    # the copied-out layout is the float layout widened to double: same terms
+    want = oracle.sps_counter(go, lay, 7, 20)
+    assert (got.mean, got.n, got.std_dev, got.skipped) == (want.mean, want.n, want.std_dev, want.skipped)
+
+
+def test_sps_perfect_layout_is_zero(pgl, gpu):
+    g = pgl.generate_synthetic_pangenome(2, 80, 2, 0.0)
+    lay = np.zeros(4 * g.n_nodes)
+    for p in g.path_steps:  # perfect_layout (test_metrics.cpp:106-116)
+        lay[4 * p["node_id"].astype(np.int64)] = p["offset"]
+        lay[4 * p["node_id"].astype(np.int64) + 2] = p["offset"] + p["seq_len"]
+    r = pgl.sampled_path_stress(g, lay, 7)
+    assert r.mean == 0.0 and r.std_dev == 0.0 and r.ci_low == 0.0 and r.ci_high == 0.0
+    assert r.n + r.skipped == 100 * 2 * 80
+
+
+def test_sps_counter_agrees_with_reference_estimator(pgl, oracle, gpu):
+    """Two-sample z-test (test_metrics.cpp:308-327) between the GPU estimate
+    and the reference's own stream on the same layouts."""
+    agree = 0
+    g, go = both(pgl, oracle, (31, 120, 2, 0.1))
+    lay, _ = oracle.run_layout(go, make_cfg(n_iters=6))
+    for k in range(40):
+        a = pgl.sampled_path_stress(g, lay, 1000 + k)
+        b = oracle.sps(go, lay, 1000 + k)
+        se = np.hypot(a.std_dev / np.sqrt(a.n), b.std_dev / np.sqrt(b.n))
+        agree += abs(a.mean - b.mean) <= 1.96 * se
+    assert agree >= 34  # ~38 expected at the 95% level
+
+
+def test_sps_rejects_zero_budget(pgl, gpu):
+    g = pgl.generate_synthetic_pangenome(2, 20, 1, 0.0)
+    with pytest.raises(pgl.InvalidParameter):
+        pgl.sampled_path_stress(g, pgl.init_layout(g, 1), 1, 0)
+
+
+# ---- Hogwild engine ---------------------------------------------------------------
+
+@pytest.mark.parametrize("drf,srf", [(1, 1), (1, 2), (2, 2), (4, 4), (2, 1)])
+def test_hogwild_accounting(pgl, gpu, drf, srf):
+    g = pgl.generate_synthetic_pangenome(12, 50, 2, 0.1)
+    budget = 10 * g.total_steps()
+    cfg = pgl.LayoutConfig(n_iters=3, drf=drf, srf=srf)
+    st = pgl.RunStats()
+    (pgl.run_layout if drf == 1 else pgl.run_layout_reuse)(g, cfg, stats=st)
+    assert st.primary_steps == cfg.n_iters * (budget // srf)
+    assert st.updates_attempted == st.primary_steps * drf
+    assert st.updates_applied + st.updates_skipped == st.updates_attempted
+    assert st.updates_applied > 0
+
+
+def test_hogwild_cooling_fractions(pgl, gpu):
+    g = pgl.generate_synthetic_pangenome(13, 500, 2, 0.0)
+    st = pgl.RunStats()
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=30, batch_size=1), stats=st)
+    spi = 10 * g.total_steps()
+    assert st.batches_first_half == 15 * spi
+    assert st.batches_second_half == 15 * spi
+    assert st.batches_second_half_cooling == st.batches_second_half
+    assert abs(st.batches_first_half_cooling / st.batches_first_half - 0.5) <= 0.01
+
+
+@pytest.mark.parametrize("n_iters", [1, 2, 3])
+def test_hogwild_switch_point(pgl, gpu, n_iters):
+    g = pgl.generate_synthetic_pangenome(14, 40, 1, 0.0)
+    spi = 10 * g.total_steps()
+    st = pgl.RunStats()
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters, batch_size=1), stats=st)
+    assert st.batches_second_half == (n_iters // 2) * spi
+    assert st.batches_first_half == n_iters * spi - (n_iters // 2) * spi
+
+
+def test_hogwild_batches_count_per_warp(pgl, gpu):
+    """batch_size 32: every warp's share opens ceil(share/32) batches."""
+    g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
+    st = pgl.RunStats()
+    with pgl.DeviceGraph(g) as dg:
+        dg.layout(pgl.LayoutConfig(n_iters=2), stats=st)
+        warps = dg.timing().device_threads // 32
+    spi = 10 * g.total_steps()
+    share, rem = divmod(spi, warps)
+    per_iter = rem * -(-(share + 1) // 32) + (warps - rem) * -(-share // 32)
+    assert st.batches_first_half == per_iter and st.batches_second_half == per_iter
+
+
+def test_hogwild_converges_and_finite(pgl, oracle, gpu):
+    g, go = both(pgl, oracle, (3, 400, 3, 0.05))
+    out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=21))
+    assert np.isfinite(out).all()
+    init = oracle.sps(go, oracle.init_layout(go, 21), 5).mean
+    assert oracle.sps(go, out, 5).mean < init / 10.0
+
+
+def test_hogwild_callback_monotone(pgl, oracle, gpu):
+    """test_engine.cpp:335-350: SPS falls along the schedule."""
+    g, go = both(pgl, oracle, (3, 400, 3, 0.05))
+    sps = [oracle.sps(go, oracle.init_layout(go, 21), 5).mean]
+
+    def cb(it, coords, eta, secs):
+        assert np.isfinite(coords).all() and secs >= 0.0
+        if it in (0, 7, 14, 29):
+            sps.append(oracle.sps(go, coords, 5).mean)
+
+    pgl.run_layout(g, pgl.LayoutConfig(global_seed=21), on_iteration=cb)
+    assert len(sps) == 5
+    for a, b in zip(sps, sps[1:]):
+        assert b <= a * 1.10
+    assert sps[-1] < sps[0] / 10.0
+
+
+def test_short_paths_tolerated(pgl, gpu):
+    g = pgl.build_graph([2, 2, 2], [[(0, 0)], [(1, 0), (2, 0)]])
+    st = pgl.RunStats()
+    out = pgl.run_layout(g, pgl.LayoutConfig(n_iters=2), stats=st)
+    assert np.isfinite(out).all() and st.updates_skipped > 0 and st.updates_applied > 0
+
+
+def test_validation_errors(pgl, gpu):
+    g = pgl.build_graph([5, 3], [[(0, 0), (1, 0)]])
+    with pytest.raises(pgl.DegenerateGraph):
+        pgl.run_layout(pgl.build_graph([5], [[(0, 0)]]))
+    with pytest.raises(pgl.DegenerateGraph):
+        pgl.run_layout(pgl.build_graph([5], []))
+    for bad in [dict(drf=3), dict(threads=0), dict(batch_size=0), dict(n_iters=0),
+                dict(zipf_theta=0.0), dict(zipf_space_max=0), dict(eta_min_eps=0.0), dict(srf=0)]:
+        with pytest.raises(pgl.InvalidParameter):
+            pgl.run_layout(g, pgl.LayoutConfig(**bad))
+    with pytest.raises(pgl.InvalidParameter):
+        pgl.run_layout_reuse(g, pgl.LayoutConfig(drf=1))
+    with pytest.raises(pgl.InvalidParameter):
+        pgl.run_layout_reuse(g, pgl.LayoutConfig(drf=3))
+
+
+def test_callback_exception_propagates(pgl, gpu):
+    g = pgl.generate_synthetic_pangenome(15, 40, 1, 0.0)
+
+    class Stop(Exception):
+        pass
+
+    def cb(it, c, eta, s):
+        if it == 2:
+            raise Stop()
+
+    with pytest.raises(Stop):
+        pgl.run_layout(g, pgl.LayoutConfig(n_iters=6), on_iteration=cb)
+
+
+@pytest.mark.slow
+def test_hogwild_sps_parity_config1(pgl, oracle, ref, gpu):
+    """North-star gate on config 1: median SPS over layout seeds 101..105
+    (metric seed 7, spn 100, the reference estimator for both sides) within
+    2% of the reference's threads=1 layouts."""
+    g = pgl.generate_synthetic_pangenome(*C1)
+    gr = ref.generate(*C1, gfa_roundtrip=True)
+    gpu_sps, cpu_sps = [], []
+    for seed in range(101, 106):
+        out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=seed))
+        gpu_sps.append(ref.sps(gr, out, 7, 100).mean)
+        lay, _ = ref.run_layout(gr, make_cfg(global_seed=seed))
+        cpu_sps.append(ref.sps(gr, lay, 7, 100).mean)
+    ratio = np.median(gpu_sps) / np.median(cpu_sps)
+    assert 0.98 <= ratio <= 1.02, (gpu_sps, cpu_sps, ratio)
