@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""bench.py — PG-SGD layout throughput on B200 (BASELINE.json metric).
+
+Workload (N=1): config 2 of BASELINE.json, the synthetic 1M-node, 90-path
+graph generate_synthetic_pangenome(1, 968000, 90, 0.05) (1,000,240 nodes,
+87,114,705 path steps), LayoutConfig{} defaults (30 iterations, theta 0.99,
+Zipf window 1000, batch 32, drf = srf = 1). One bench step = one full
+run_layout of that graph: 30 x 10 x sum|p| = 2.61e10 attempted updates.
+
+  value  : updates/s with the packed graph resident in HBM; device time from
+           CUDA events on the library's stream (init upload -> last SGD
+           kernel), L2 flushed between steps.
+  e2e    : updates/s through the C-ABI drop-in pgl_layout_run with HOST
+           buffers: pack + H2D of the graph and initial layout, 30 kernels,
+           D2H of the coordinates, every step (host wall, synchronised).
+  roofline: k_sgd_hogwild, 192 algorithmic bytes per update (6 random
+           32-byte sectors) x updates per launch / mean
+           launch time, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline: the reference library itself (oracle/_ref, built from the
+           reference sources), all host cores, on a bounded sample.
+
+--gpus N (torchrun): every rank lays out its own copy of the graph (one
+chromosome per GPU, no collective: SURVEY.md §8e) -> weak scaling;
+value = all ranks' updates / max-over-ranks time.
+--impl reference: times the reference CPU implementation (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PG-SGD updates/sec and layout wall-time per chromosome; sampled path stress"
+UNIT = "updates/s"
+BYTES_PER_UPDATE = 192  # 6 random 32-byte sectors
+CONFIGS = {
+    "c1": (1, 9680, 8, 0.05),
+    "c2": (1, 968000, 90, 0.05),
+    "c3": (1, 9680000, 90, 0.05),
+}
+WORKLOAD_NAME = {
+    "c1": "config 1: synthetic ~10k-node 8-path graph (generate_synthetic_pangenome(1, 9680, 8, 0.05)), 30 iters",
+    "c2": "config 2: synthetic 1M-node 90-path graph (generate_synthetic_pangenome(1, 968000, 90, 0.05)), 30 iters",
+    "c3": "config 3: chr1-scale synthetic 10M-node 90-path graph (generate_synthetic_pangenome(1, 9680000, 90, 0.05)), 30 iters",
+}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--coord", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# ---- distributed plumbing (torch.distributed is plumbing only) -------------------
+
+class Dist:
+    def __init__(self, n_gpus: int):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist, self.torch, self.backend = dist, torch, backend
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64,
+                              device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64,
+                              device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def aggregate(dist: Dist, per_rank_units: float, per_rank_seconds: float):
+    """Whole-job throughput: all ranks' units over the slowest rank's time."""
+    t = dist.max(per_rank_seconds)
+    units = dist.sum(per_rank_units)
+    return units / t if t > 0 else 0.0, t
+
+
+# ---- clocks sampler -------------------------------------------------------------
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+class Clocks:
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows
+        busy = [r for r in rows if not (r[2] & 0x1)] or rows
+        reasons = set()
+        for r in busy:
+            for bit, name in REASON_BITS.items():
+                if r[2] & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[0] for r in busy) if busy else None,
+                "sm_max_mhz": max(r[1] for r in busy) if busy else None,
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ---- peaks, profiles ------------------------------------------------------------
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config: str, coord: str):
+    """dram bytes per SGD launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d[f"{config}_{coord}"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+# ---- CPU baseline: the reference itself --------------------------------------------
+
+def cpu_reference_sample(args, n_steps_total=1, budget_s=20.0):
+    """Times pglref::run_layout (oracle/_ref, the reference's own sources) with
+    threads = all host cores on a bounded sample of the workload: 2 iterations
+    (one mixed, one forced-cooling, as SURVEY.md §8d extrapolates) with srf
+    chosen so each sample takes ~budget_s. Returns (updates/s, cores, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ffi import REF_SO, Reference, make_cfg  # checker infrastructure
+    kind = "reference"
+    if not os.path.exists(REF_SO):
+        return None
+    R = Reference()
+    seed, bb, paths, rate = CONFIGS[args.config]
+    g = R.generate(seed, bb, paths, rate, gfa_roundtrip=(args.config == "c1"))
+    cores = os.cpu_count() or 1
+    # ~1.5 M updates/s per core measured for the reference at this scale
+    est_rate = 1.5e6 * cores
+    per_iter_full = 10 * g.total_steps
+    want = max(est_rate * budget_s / 2.0, 2e6)
+    srf = max(1, int(math.ceil(per_iter_full / want)))
+    cfg = make_cfg(n_iters=2, threads=cores, srf=srf, global_seed=101)
+    rates = []
+    sample = None
+    for _ in range(n_steps_total):
+        t0 = time.perf_counter()
+        _, st = R.run_layout(g, cfg)
+        dt = time.perf_counter() - t0
+        rates.append(st.updates_attempted / dt)
+        sample = (f"{args.config} graph, run_layout with n_iters=2 (mixed + forced-cooling iteration), "
+                  f"srf={srf} -> {st.updates_attempted} updates per sample, threads={cores}")
+    return statistics.median(rates), cores, sample, kind, rates
+
+
+def run_reference_arm(args, dist: Dist):
+    if dist.rank != 0:
+        return
+    steps = args.steps + args.warmup
+    budget = max(3.0, min(args.cpu_budget_s, 150.0 / max(steps, 1)))
+    res = cpu_reference_sample(args, n_steps_total=steps, budget_s=budget)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpglref.so not built"}))
+        return
+    _, cores, sample, kind, rates = res
+    timed = rates[args.warmup:] or rates
+    v = statistics.median(timed)
+    seed, bb, paths, rate = CONFIGS[args.config]
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD_NAME[args.config], "threads": cores},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ---- our arm ----------------------------------------------------------------------
+
+def run_ours(args, dist: Dist):
+    import paper_2409_00876_b200 as P
+    import torch
+
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
+
+    seed, bb, paths, rate = CONFIGS[args.config]
+    g = P.generate_synthetic_pangenome(seed, bb, paths, rate)
+    S = g.total_steps()
+    cfg = P.LayoutConfig(global_seed=42 + dist.rank)
+    ext = P.LayoutExt(coord_precision=P.COORD_F64 if args.coord == "f64" else P.COORD_F32)
+    updates = cfg.n_iters * (10 * S // cfg.srf) * cfg.drf
+
+    dg = P.DeviceGraph(g, device=dev)
+    for _ in range(args.warmup):
+        dg.layout(cfg, ext=ext, copy_out=False)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(dev)
+    clocks.start()
+    dev_ms, kern_ms, launches = [], [], 0
+    dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dg.layout(cfg, ext=ext, copy_out=False)
+        tm = dg.timing()
+        dev_ms.append(tm.device_ms)
+        kern_ms.append(tm.kernel_ms)
+        launches += tm.launches + 2  # 30 SGD + seed_rng + f64->f32 init narrowing
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    step_s = sum(dev_ms) / 1e3 / args.steps
+    value, t_max = aggregate(dist, updates * args.steps, step_s * args.steps)
+    sgd_launch_ms = sum(kern_ms) / (args.steps * cfg.n_iters)
+
+    # quality of the bench's own layout (device SPS kernel, spn 100, seed 7)
+    sps, sps_ms = dg.stress(7, 100, return_ms=True)
+    timing = dg.timing()
+    info = dg.info()
+    dg.close()
+
+    # e2e through the C-ABI drop-in with host buffers
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3))
+    P.run_layout(g, cfg, ext=ext, device=dev)  # warm
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        P.run_layout(g, cfg, ext=ext, device=dev)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    dist.barrier()
+    e2e_val, _ = aggregate(dist, updates * e2e_steps, e2e_s * e2e_steps)
+    h2d = 16 * S + 8 * (g.n_paths + 1) + 48 * g.n_paths + 32 * g.n_nodes + 4 * (1 << 16)
+    d2h = 32 * g.n_nodes + 64
+
+    cpu = None
+    if dist.rank == 0 and not args.no_cpu_baseline and args.gpus == 1:
+        res = cpu_reference_sample(args, 1, args.cpu_budget_s)
+        if res:
+            v, cores, sample, kind, _ = res
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+
+    peak, peak_src = hbm_peak()
+    bytes_per_launch = (10 * S // cfg.srf) * cfg.drf * BYTES_PER_UPDATE
+    achieved = bytes_per_launch / (sgd_launch_ms / 1e3) / 1e9
+    traffic = ncu_traffic(args.config, args.coord)
+    if dist.rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAME[args.config], "nodes": g.n_nodes, "paths": g.n_paths,
+                       "path_steps": S, "iters": cfg.n_iters, "updates_per_step": updates,
+                       "coord_storage": args.coord, "parallelism": f"graph-per-GPU x{args.gpus} (no collective)",
+                       "l2": "flushed between steps (256 MiB write); graph index 16 B/step > L2",
+                       "lanes": timing.device_threads, "grid": [timing.grid_blocks, timing.block_threads]},
+            "layout_wall_s": t_max / args.steps,
+            "sps": {"mean": sps.mean, "ci": [sps.ci_low, sps.ci_high], "n": sps.n,
+                    "method": "counter (GPU), seed 7, 100 samples/step", "kernel_ms": sps_ms},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "seconds_per_step": e2e_s, "api": "pgl_layout_run (C-ABI) from host PathStep arrays"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgd_hogwild",
+                         "bytes_per_update": BYTES_PER_UPDATE, "launch_ms": sgd_launch_ms,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "device_bytes": info["device_bytes"],
+        }
+        print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    dist = Dist(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -233,6 +233,8 @@ typedef struct pgl_timing {
     double kernel_ms;      /* sum over SGD launches */
     double init_ms;        /* host init_layout + upload of the initial layout */
     double total_ms;       /* whole call, host wall */
+    double device_ms;      /* CUDA events on the graph's stream: from the upload of
+                              the initial layout to the end of the last SGD kernel */
     uint32_t launches;     /* SGD kernel launches (one per iteration) */
     uint32_t grid_blocks;
     uint32_t block_threads;

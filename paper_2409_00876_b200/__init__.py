@@ -103,7 +103,7 @@ class _Info(C.Structure):
 
 class _Timing(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("init_ms", C.c_double), ("total_ms", C.c_double),
-                ("launches", C.c_uint32), ("grid_blocks", C.c_uint32), ("block_threads", C.c_uint32),
+                ("device_ms", C.c_double), ("launches", C.c_uint32), ("grid_blocks", C.c_uint32), ("block_threads", C.c_uint32),
                 ("_pad0", C.c_uint32), ("device_threads", C.c_uint64)]
 
 
@@ -277,6 +277,7 @@ class Timing:
     kernel_ms: float
     init_ms: float
     total_ms: float
+    device_ms: float
     launches: int
     grid_blocks: int
     block_threads: int
@@ -545,7 +546,7 @@ class DeviceGraph:
     def timing(self) -> Timing:
         t = _Timing()
         _check(_lib.pgl_graph_last_timing(self.h, C.byref(t)))
-        return Timing(t.kernel_ms, t.init_ms, t.total_ms, t.launches, t.grid_blocks, t.block_threads,
+        return Timing(t.kernel_ms, t.init_ms, t.total_ms, t.device_ms, t.launches, t.grid_blocks, t.block_threads,
                       t.device_threads)
 
     def stress(self, seed: int, samples_per_node: int = 100, layout: Optional[np.ndarray] = None,

@@ -473,6 +473,10 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     double* hinit = static_cast<double*>(G->pin.p);
     init_layout(&hv, G->sum.total_nt, cfg.global_seed, hinit);
     G->coords64.alloc(4 * V);
+    cudaEvent_t ev_begin, ev_end;
+    PGL_CUDA(cudaEventCreate(&ev_begin));
+    PGL_CUDA(cudaEventCreate(&ev_end));
+    PGL_CUDA(cudaEventRecord(ev_begin, G->stream));
     PGL_CUDA(cudaMemcpyAsync(G->coords64.p, hinit, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
     void* coords = G->coords64.p;
     if (!f64) {
@@ -584,8 +588,16 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             if (cb(it, cptr, a.eta, now_s() - t_it, user) != 0) aborted = true;
         }
     }
+    PGL_CUDA(cudaEventRecord(ev_end, G->stream));
     PGL_CUDA(cudaStreamSynchronize(G->stream));
     G->layout_f64 = f64;
+    {
+        float dms = 0.f;
+        cudaEventElapsedTime(&dms, ev_begin, ev_end);
+        G->timing.device_ms = dms;
+        cudaEventDestroy(ev_begin);
+        cudaEventDestroy(ev_end);
+    }
     double kms = 0.0;
     uint32_t launches = 0;
     for (uint32_t it = 0; it < cfg.n_iters; ++it) {
