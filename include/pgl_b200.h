@@ -123,8 +123,9 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t steps_per_thread_ilp; /* reserved, 0 */
-    uint32_t _reserved[9];
+    uint32_t kernel_variant;  /* 0 = 2 CTAs/SM, no spills; 1 = 3 CTAs/SM (80 regs) */
+    uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
+    uint32_t _reserved[8];
 } pgl_layout_ext;
 
 void pgl_layout_ext_default(pgl_layout_ext* ext);

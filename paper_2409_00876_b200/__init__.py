@@ -68,7 +68,8 @@ class _Cfg(C.Structure):
 class _Ext(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("mode", C.c_uint32), ("coord_precision", C.c_uint32),
                 ("max_warps", C.c_uint32), ("block_threads", C.c_uint32), ("l2_persist", C.c_uint32),
-                ("steps_per_thread_ilp", C.c_uint32), ("_reserved", C.c_uint32 * 9)]
+                ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
+                ("_reserved", C.c_uint32 * 8)]
 
 
 class _PathStep(C.Structure):
@@ -226,12 +227,16 @@ class LayoutExt:
     max_warps: int = 0
     block_threads: int = 0
     l2_persist: int = 0
+    l2_fetch_bytes: int = 0
+    kernel_variant: int = 0
 
     def _c(self) -> _Ext:
         e = _Ext()
         _lib.pgl_layout_ext_default(C.byref(e))
         e.mode, e.coord_precision = self.mode, self.coord_precision
         e.max_warps, e.block_threads, e.l2_persist = self.max_warps, self.block_threads, self.l2_persist
+        e.l2_fetch_bytes = self.l2_fetch_bytes
+        e.kernel_variant = self.kernel_variant
         return e
 
 

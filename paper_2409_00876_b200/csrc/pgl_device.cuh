@@ -241,4 +241,98 @@ __device__ __forceinline__ uint32_t pgsgd_step(const DevGraph& g, void* coords, 
     return applied;
 }
 
+// ---- Hogwild fast path helpers -------------------------------------------------
+// The Hogwild kernel does not need to reproduce the reference's rounding (its
+// races already make it nondeterministic), so it avoids every call into the
+// IEEE division/sqrt slow paths: those CALLs force the loop state through the
+// stack. Reciprocal and reciprocal square root start from the MUFU 64-bit
+// approximations and are refined by Newton steps to ~1 ulp.
+
+__device__ __forceinline__ double rcp_nr(double b) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+    double e = fma(-b, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-b, y, 1.0);
+    return fma(y, e, y);
+}
+
+__device__ __forceinline__ double rsqrt_nr(double s) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+    const double h = 0.5 * s;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// Step record gather, streaming: read-only path, no L1 allocation, L2
+// evict-first so the one-touch records do not push the coordinates out.
+__device__ __forceinline__ StepRec load_step_stream(const StepRec* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return StepRec{v.x, v.y, v.z, v.w};
+}
+
+// Coordinate endpoint access through L2 (.cg) with an evict-last policy: the
+// coordinate array is the reused working set (1.7k touches per node per
+// iteration at config 2) and should stay L2-resident.
+template <typename T> struct CoordHint;
+
+template <> struct CoordHint<float> {
+    __device__ __forceinline__ static void get(const void* base, uint32_t node, int end, uint64_t pol,
+                                               double& x, double& y) {
+        const float2* a = reinterpret_cast<const float2*>(base) + 2 * static_cast<uint64_t>(node) + end;
+        float fx, fy;
+        asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(fx), "=f"(fy) : "l"(a), "l"(pol));
+        x = fx;
+        y = fy;
+    }
+    __device__ __forceinline__ static void set(void* base, uint32_t node, int end, uint64_t pol, double x,
+                                               double y) {
+        float2* a = reinterpret_cast<float2*>(base) + 2 * static_cast<uint64_t>(node) + end;
+        asm volatile("st.global.cg.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;"
+                     :: "l"(a), "f"(static_cast<float>(x)), "f"(static_cast<float>(y)), "l"(pol) : "memory");
+    }
+};
+
+template <> struct CoordHint<double> {
+    __device__ __forceinline__ static void get(const void* base, uint32_t node, int end, uint64_t pol,
+                                               double& x, double& y) {
+        const double2* a = reinterpret_cast<const double2*>(base) + 2 * static_cast<uint64_t>(node) + end;
+        asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                     : "=d"(x), "=d"(y) : "l"(a), "l"(pol));
+    }
+    __device__ __forceinline__ static void set(void* base, uint32_t node, int end, uint64_t pol, double x,
+                                               double y) {
+        double2* a = reinterpret_cast<double2*>(base) + 2 * static_cast<uint64_t>(node) + end;
+        asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" :: "l"(a), "d"(x), "d"(y), "l"(pol)
+                     : "memory");
+    }
+};
+
+// Zipf(zn, theta) on [1, zn] by Walker's alias method: one 64-bit draw, the
+// column from its high word, the keep/alias test on its low word. The table
+// is built on the host from the exact pmf k^-theta / H(zn, theta), so the
+// distribution is the one ZipfSampler (rng.hpp:103-117) samples.
+__device__ __forceinline__ uint64_t zipf_alias(const ZipfAlias* tab, uint32_t zn, uint64_t x) {
+    const uint32_t col = __umulhi(static_cast<uint32_t>(x >> 32), zn);
+    const uint2 e = __ldg(reinterpret_cast<const uint2*>(tab) + col);
+    return 1 + (static_cast<uint32_t>(x) < e.x ? col : e.y);
+}
+
 }  // namespace pgl

@@ -277,6 +277,37 @@ void finish_report(pgl_stress_report* r, double ssd) {  // metrics.cpp:14-23
     r->ci_high = r->mean + half;
 }
 
+// Walker/Vose alias table for Zipf(zn, theta) on [1, zn] with the exact pmf
+// k^-theta / H(zn, theta) that the rejection-inversion sampler targets
+// (rng.hpp:83-151). Appended to `out`; thresholds are P(keep) * 2^32.
+void append_zipf_alias(uint64_t zn, double theta, std::vector<ZipfAlias>& out) {
+    if (zn > (1ULL << 24)) raise(PGL_ERR_INVALID_PARAMETER, "zipf support above 2^24 is not supported by the GPU sampler");
+    const size_t n = static_cast<size_t>(zn), off = out.size();
+    std::vector<double> q(n);
+    double h = 0.0, comp = 0.0;  // Kahan sum of k^-theta, smallest terms first
+    for (size_t k = n; k >= 1; --k) {
+        const double t = std::pow(static_cast<double>(k), -theta) - comp;
+        const double s2 = h + t;
+        comp = (s2 - h) - t;
+        h = s2;
+    }
+    for (size_t k = 0; k < n; ++k) q[k] = std::pow(static_cast<double>(k + 1), -theta) / h * static_cast<double>(n);
+    out.resize(off + n);
+    std::vector<uint32_t> small, large;
+    for (size_t k = 0; k < n; ++k) (q[k] < 1.0 ? small : large).push_back(static_cast<uint32_t>(k));
+    while (!small.empty() && !large.empty()) {
+        const uint32_t sm = small.back(), lg = large.back();
+        small.pop_back();
+        large.pop_back();
+        const double t = q[sm] * 4294967296.0;
+        out[off + sm] = ZipfAlias{static_cast<uint32_t>(std::min(t, 4294967295.0)), lg};
+        q[lg] = (q[lg] + q[sm]) - 1.0;
+        (q[lg] < 1.0 ? small : large).push_back(lg);
+    }
+    for (uint32_t k : large) out[off + k] = ZipfAlias{0xFFFFFFFFu, k};
+    for (uint32_t k : small) out[off + k] = ZipfAlias{0xFFFFFFFFu, k};  // rounding leftovers
+}
+
 }  // namespace pgl
 
 using namespace pgl;
@@ -295,6 +326,7 @@ struct pgl_graph {
     DevBuf<uint64_t> cum;
     DevBuf<uint32_t> guide;
     DevBuf<PathConst> pc;
+    DevBuf<ZipfAlias> zalias;
     uint32_t guide_bits = 8;
     DevBuf<double> coords64;             // [4V] FP64 layout / staging
     DevBuf<float> coords32;              // [4V] FP32 layout
@@ -318,6 +350,7 @@ struct pgl_graph {
         d.cum = cum.p;
         d.guide = guide.p;
         d.pc = pc.p;
+        d.zalias = zalias.p;
         d.total_steps = sum.total_steps;
         d.n_paths = n_paths;
         d.guide_bits = guide_bits;
@@ -486,32 +519,40 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     }
 
     // per-path constants for this config (zipf_params_for, engine.cpp:36-39)
+    // plus one alias table per distinct Zipf support for the Hogwild kernel.
     std::vector<PathConst> pcs(G->n_paths);
+    std::vector<ZipfAlias> tables;
     {
         uint64_t base = 0;
-        std::vector<std::pair<uint64_t, std::array<double, 3>>> memo;
+        struct Memo {
+            uint64_t zn;
+            double k[3];
+            uint64_t off;
+        };
+        std::vector<Memo> memo;
         for (uint32_t p = 0; p < G->n_paths; ++p) {
             const uint64_t n = G->path_n_steps[p];
             const uint64_t span = n < 2 ? 1 : n - 1;
             const uint64_t zn = std::min<uint64_t>(span, cfg.zipf_space_max);
-            PathConst c{base, n, zn, 0, 0, 0};
-            auto it = std::find_if(memo.begin(), memo.end(), [&](auto& m) { return m.first == zn; });
+            auto it = std::find_if(memo.begin(), memo.end(), [&](const Memo& m) { return m.zn == zn; });
             if (it == memo.end()) {
-                std::array<double, 3> k;
-                zipf_constants(zn, cfg.zipf_theta, &k[0], &k[1], &k[2]);
-                memo.emplace_back(zn, k);
+                Memo m{zn, {0, 0, 0}, tables.size()};
+                zipf_constants(zn, cfg.zipf_theta, &m.k[0], &m.k[1], &m.k[2]);
+                if (!replay) append_zipf_alias(zn, cfg.zipf_theta, tables);
+                memo.push_back(m);
                 it = memo.end() - 1;
             }
-            c.hx1 = it->second[0];
-            c.hxn = it->second[1];
-            c.s = it->second[2];
-            pcs[p] = c;
+            pcs[p] = PathConst{base, n, zn, it->k[0], it->k[1], it->k[2], it->off};
             base += n;
         }
     }
     G->pc.alloc(pcs.size());
     PGL_CUDA(cudaMemcpyAsync(G->pc.p, pcs.data(), pcs.size() * sizeof(PathConst), cudaMemcpyHostToDevice,
                              G->stream));
+    G->zalias.alloc(std::max<size_t>(tables.size(), 1));
+    if (!tables.empty())
+        PGL_CUDA(cudaMemcpyAsync(G->zalias.p, tables.data(), tables.size() * sizeof(ZipfAlias),
+                                 cudaMemcpyHostToDevice, G->stream));
     PGL_CUDA(cudaMemsetAsync(G->stats.p, 0, 8 * sizeof(unsigned long long), G->stream));
 
     // RNG states: lane t <- seed_worker(seed, t) (rng.hpp:63-71)
@@ -520,7 +561,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     uint64_t lanes = 1;
     if (!replay) {
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
-        shape = sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads));
+        shape = sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant));
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -552,6 +593,11 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     PGL_CUDA(cudaStreamSynchronize(G->stream));
     const double init_ms = (now_s() - t_init) * 1e3;
 
+    // Random 16-byte record gathers: fetch exactly one 32-byte sector per L2
+    // miss instead of the default promoted line (restored below).
+    size_t prev_gran = 0;
+    cudaDeviceGetLimit(&prev_gran, cudaLimitMaxL2FetchGranularity);
+    if (!replay) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, ext.l2_fetch_bytes ? ext.l2_fetch_bytes : 32);
     const uint64_t spi = 10 * G->sum.total_steps / cfg.srf;  // engine.cpp:197
     const DevGraph dg_ = G->dev();
     DevStats* dstats = reinterpret_cast<DevStats*>(G->stats.p);
@@ -608,6 +654,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         }
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    if (!replay && prev_gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, prev_gran);
     if (aborted) raise(PGL_ERR_CALLBACK, "iteration callback requested abort");
 
     unsigned long long dst[8];

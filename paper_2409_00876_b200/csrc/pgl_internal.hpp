@@ -46,6 +46,14 @@ struct alignas(16) PathConst {
     uint64_t n;       // |p|
     uint64_t zn;      // Zipf support n = min(max(|p|-1,1), zipf_space_max)
     double hx1, hxn, s;
+    uint64_t ztab;    // offset of this support's alias table in DevGraph::zalias
+};
+
+// Walker/Vose alias table entry for Zipf(zn, theta) on [1, zn]: column c is
+// kept when the 32-bit threshold test passes, else replaced by alias.
+struct ZipfAlias {
+    uint32_t thresh;  // P(keep column) * 2^32 (saturating)
+    uint32_t alias;   // 0-based alternative column
 };
 
 // Everything a kernel needs to read the resident graph.
@@ -54,6 +62,7 @@ struct DevGraph {
     const uint64_t* cum;      // [P+1]
     const uint32_t* guide;    // [1 << guide_bits] path of the bucket's first pick
     const PathConst* pc;      // [P]
+    const ZipfAlias* zalias;  // alias tables, one per distinct Zipf support
     uint64_t total_steps;
     uint32_t n_paths;
     uint32_t guide_bits;
@@ -88,10 +97,11 @@ struct DevStats {
 struct LaunchShape {
     int blocks = 0;
     int threads = 256;
+    int variant = 0;
 };
 
 // Occupancy-derived persistent grid for the Hogwild kernel.
-LaunchShape sgd_shape(int device, int coord_f64, uint32_t max_warps, int block_threads);
+LaunchShape sgd_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant);
 
 void launch_seed_rng(DevRng rng, uint64_t n_lanes, uint64_t seed, void* stream);
 void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng rng,
@@ -123,5 +133,6 @@ void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);
 
 void zipf_constants(uint64_t n, double theta, double* hx1, double* hxn, double* s);
 void finish_report(pgl_stress_report* r, double sum_sq_dev);
+void append_zipf_alias(uint64_t zn, double theta, std::vector<ZipfAlias>& out);
 
 }  // namespace pgl

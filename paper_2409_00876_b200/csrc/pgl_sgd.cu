@@ -40,8 +40,141 @@ __device__ __forceinline__ void flush_stats(DevStats* st, int idx, uint32_t v) {
     if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&st->v[idx], static_cast<unsigned long long>(sum));
 }
 
+// One selected step pair in flight between the two pipeline stages.
+struct Sel {
+    StepRec ri, rj;
+    uint32_t flags;  // bit0 valid, bit1 e_i is end, bit2 e_j is end
+};
+
+// Stage A (warp-uniform call): the batch decision of engine.cpp:115-124 for
+// this round, then select_step_pair (:52-80) and the two endpoint coins, and
+// issue the two step-record gathers. Nothing waits on the gathers here.
+template <bool kActiveCheck>
+__device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const IterArgs& a, uint64_t base,
+                                            uint64_t count, uint32_t lane, bool& carry, uint32_t& b_first,
+                                            uint32_t& b_first_cool, uint32_t& b_second, uint64_t pol_stream) {
+    const uint64_t s = base + lane;
+    const bool active = s < count;
+    const uint64_t in_batch = s % a.batch;
+    bool mine = false;
+    if (active && in_batch == 0) {
+        if (a.force_cooling) {
+            mine = true;
+            ++b_second;
+        } else {
+            mine = r.coin();
+            ++b_first;
+            b_first_cool += mine;
+        }
+    }
+    const int opener = in_batch <= lane ? static_cast<int>(lane - in_batch) : -1;
+    const bool opened = __shfl_sync(kFull, mine, opener < 0 ? 0 : opener);
+    const bool cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
+    carry = __shfl_sync(kFull, cooling, 31);
+
+    Sel out;
+    out.flags = 0;
+    out.ri = out.rj = StepRec{0, 0, 0, 0};
+    if (!active) return out;
+    const uint64_t x = r.next();
+    const uint64_t pick = __umul64hi(x, g.total_steps);
+    const uint32_t p = select_path(g, x, pick);
+    const uint64_t pbase = __ldg(g.cum + p);
+    const int64_t n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
+    if (n < 2) return out;
+    const int64_t i = static_cast<int64_t>(pick - pbase);
+    int64_t j;
+    uint64_t bits;
+    if (cooling) {
+        const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
+        const uint64_t zt = __ldg(&g.pc[p].ztab);
+        const int64_t k = static_cast<int64_t>(zipf_alias(g.zalias + zt, zn, r.next()));
+        bits = r.next();
+        const int64_t sign = (bits >> 61) & 1 ? 1 : -1;
+        j = i + sign * k;
+        if (j < 0 || j >= n) {
+            j = i - sign * k;
+            if (j < 0 || j >= n) {
+                j = i + sign * k;
+                j = j < 0 ? 0 : (j > n - 1 ? n - 1 : j);
+            }
+        }
+        if (j == i) return out;
+    } else {
+        j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+        if (j == i) {
+            j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+            if (j == i) return out;
+        }
+        bits = r.next();
+    }
+    out.ri = load_step_stream(g.step + pbase + i, pol_stream);
+    out.rj = load_step_stream(g.step + pbase + j, pol_stream);
+    // coin true -> Endpoint::start (engine.cpp:89-91): a set bit means start
+    out.flags = 1u | ((bits >> 63) ? 0u : 2u) | (((bits >> 62) & 1) ? 0u : 4u);
+    return out;
+}
+
+// apply_endpoint_update (engine.cpp:276-306) on the Hogwild store, without
+// calls into IEEE slow paths. Returns 1 if applied.
 template <typename T>
-__global__ void __launch_bounds__(256) k_sgd_hogwild(DevGraph g, void* __restrict__ coords, DevRng rng,
+__device__ __forceinline__ uint32_t hog_update(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                               double d_ref, double eta, Xo& r, uint64_t pol) {
+    if (!(d_ref > 0.0)) return 0;
+    double mu = eta * rcp_nr(d_ref * d_ref);
+    if (mu > 1.0) mu = 1.0;
+    double vix, viy, vjx, vjy;
+    CoordHint<T>::get(coords, ni, ei, pol, vix, viy);
+    CoordHint<T>::get(coords, nj, ej, pol, vjx, vjy);
+    const double dx = vix - vjx;
+    const double dy = viy - vjy;
+    const double s2 = dx * dx + dy * dy;
+    double ux, uy, mag;
+    if (s2 < 1e-18) {  // |v_i - v_j| < 1e-9: random unit direction
+        float sn, cs;
+        sincospif(2.0f * static_cast<float>(r.uniform()), &sn, &cs);
+        ux = cs;
+        uy = sn;
+        mag = sqrt(s2);
+    } else {
+        const double rs = rsqrt_nr(s2);
+        mag = s2 * rs;
+        ux = dx * rs;
+        uy = dy * rs;
+    }
+    const double delta = mu * (mag - d_ref) * 0.5;
+    CoordHint<T>::set(coords, ni, ei, pol, vix - delta * ux, viy - delta * uy);
+    CoordHint<T>::set(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy);
+    return 1;
+}
+
+// Stage B: the update(s) of one selected pair (engine.cpp:133-170).
+template <typename T>
+__device__ __forceinline__ uint32_t stage_update(const Sel& sel, void* coords, Xo& r, const IterArgs& a,
+                                                 uint64_t pol) {
+    if (!(sel.flags & 1u)) return 0;
+    const int ei = (sel.flags >> 1) & 1, ej = (sel.flags >> 2) & 1;
+    uint32_t applied = hog_update<T>(coords, sel.ri.node, ei, sel.rj.node, ej,
+                                     abs_diff(step_pos(sel.ri, ei), step_pos(sel.rj, ej)), a.eta, r, pol);
+    if (a.drf > 1) {
+        unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+        for (uint32_t extra = 1; extra < a.drf; ++extra) {
+            int ea, eb;
+            do {
+                const uint64_t bits = r.next();
+                ea = (bits >> 63) ? 0 : 1;
+                eb = ((bits >> 62) & 1) ? 0 : 1;
+            } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+            used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+            applied += hog_update<T>(coords, sel.ri.node, ea, sel.rj.node, eb,
+                                     abs_diff(step_pos(sel.ri, ea), step_pos(sel.rj, eb)), a.eta, r, pol);
+        }
+    }
+    return applied;
+}
+
+template <typename T, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                      DevStats* stats, IterArgs a) {
     const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint32_t warp = static_cast<uint32_t>(tid >> 5);
@@ -51,29 +184,22 @@ __global__ void __launch_bounds__(256) k_sgd_hogwild(DevGraph g, void* __restric
     Xo r{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
     const uint64_t share = a.steps / a.n_warps;
     const uint64_t count = share + (warp < a.steps % a.n_warps ? 1 : 0);
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
-    bool carry = false;  // cooling flag of the batch still open at the round boundary
+    bool carry = false;
+    // Two-stage software pipeline over rounds: the step records of round
+    // r+1 are in flight while round r gathers and updates coordinates.
+    Sel cur = stage_select<true>(g, r, a, 0, count, lane, carry, b_first, b_first_cool, b_second, pol_stream);
     for (uint64_t base = 0; base < count; base += 32) {
-        const uint64_t s = base + lane;
-        const bool active = s < count;
-        const uint64_t in_batch = s % a.batch;
-        bool mine = false;
-        if (active && in_batch == 0) {  // this lane opens a batch (engine.cpp:115-124)
-            if (a.force_cooling) {
-                mine = true;
-                ++b_second;
-            } else {
-                mine = r.coin();
-                ++b_first;
-                b_first_cool += mine;
-            }
-        }
-        const int opener = in_batch <= lane ? static_cast<int>(lane - in_batch) : -1;
-        const bool opened = __shfl_sync(kFull, mine, opener < 0 ? 0 : opener);
-        const bool cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
-        carry = __shfl_sync(kFull, cooling, 31);
-        if (active) applied += pgsgd_step<T>(g, coords, r, cooling, a.eta, a.theta, a.drf);
+        Sel nxt;
+        nxt.flags = 0;
+        if (base + 32 < count)
+            nxt = stage_select<true>(g, r, a, base + 32, count, lane, carry, b_first, b_first_cool, b_second,
+                                     pol_stream);
+        applied += stage_update<T>(cur, coords, r, a, pol_keep);
+        cur = nxt;
     }
 
     rng.s0[tid] = r.a;
@@ -130,15 +256,21 @@ __global__ void k_f32_to_f64(const float* __restrict__ s, double* __restrict__ d
 
 }  // namespace
 
-LaunchShape sgd_shape(int device, int coord_f64, uint32_t max_warps, int block_threads) {
+// Kernel variants: occupancy target 2 blocks/SM (no spills) or 3 (80 regs).
+template <typename T>
+const void* hogwild_fn(int variant) {
+    return variant == 1 ? reinterpret_cast<const void*>(k_sgd_hogwild<T, 3>)
+                        : reinterpret_cast<const void*>(k_sgd_hogwild<T, 1>);
+}
+
+LaunchShape sgd_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant) {
     LaunchShape sh;
     sh.threads = block_threads > 0 ? block_threads : 256;
+    sh.variant = variant;
     int sms = 0, occ = 0;
     PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    if (coord_f64)
-        PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sgd_hogwild<double>, sh.threads, 0));
-    else
-        PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sgd_hogwild<float>, sh.threads, 0));
+    PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, coord_f64 ? hogwild_fn<double>(variant) : hogwild_fn<float>(variant), sh.threads, 0));
     if (occ < 1) occ = 1;
     uint64_t warps = static_cast<uint64_t>(sms) * occ * (sh.threads / 32);
     if (max_warps && warps > max_warps) warps = max_warps;
@@ -157,10 +289,9 @@ void launch_seed_rng(DevRng rng, uint64_t n_lanes, uint64_t seed, void* stream) 
 void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng rng, DevStats* stats,
                         const IterArgs& a, LaunchShape shape, void* stream) {
     auto s = static_cast<cudaStream_t>(stream);
-    if (coord_f64)
-        k_sgd_hogwild<double><<<shape.blocks, shape.threads, 0, s>>>(g, coords, rng, stats, a);
-    else
-        k_sgd_hogwild<float><<<shape.blocks, shape.threads, 0, s>>>(g, coords, rng, stats, a);
+    void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
+    PGL_CUDA(cudaLaunchKernel(coord_f64 ? hogwild_fn<double>(shape.variant) : hogwild_fn<float>(shape.variant),
+                              dim3(shape.blocks), dim3(shape.threads), args, 0, s));
     PGL_CUDA(cudaGetLastError());
 }
 

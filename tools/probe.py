@@ -28,6 +28,24 @@ if what in ("all", "c2"):
     rr, ms = dg.stress(7, 100, return_ms=True)
     print("sps spn100 on device: %.4g in %.1f ms" % (rr.mean, ms), flush=True)
 
+if what == "sweep":
+    t = time.time(); g = P.generate_synthetic_pangenome(1, 968000, 90, 0.05); print("gen C2 %.2fs" % (time.time() - t), flush=True)
+    dg = P.DeviceGraph(g)
+    upd = 30 * 10 * g.total_steps()
+    for prec in (0, 1):
+        for var in (0, 1):
+            for fetch in (32, 64, 128):
+                for persist in (0, 1):
+                    ext = P.LayoutExt(coord_precision=prec, kernel_variant=var, l2_fetch_bytes=fetch, l2_persist=persist)
+                    dg.layout(P.LayoutConfig(n_iters=2), ext=ext, copy_out=False)
+                    st = P.RunStats()
+                    dg.layout(P.LayoutConfig(), ext=ext, stats=st, copy_out=False)
+                    tm = dg.timing()
+                    r = dg.stress(7, 10)
+                    print(json.dumps(dict(prec=prec, var=var, fetch=fetch, persist=persist, lanes=tm.device_threads,
+                                          kernel_ms=round(tm.kernel_ms, 1), gupd=round(upd / tm.kernel_ms / 1e6, 3),
+                                          applied=round(st.updates_applied / st.updates_attempted, 5), sps10=r.mean)), flush=True)
+
 if what in ("all", "c1") and R is not None:
     g = P.generate_synthetic_pangenome(1, 9680, 8, 0.05)
     gr = R.generate(1, 9680, 8, 0.05, gfa_roundtrip=True)
