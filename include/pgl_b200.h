@@ -109,6 +109,18 @@ typedef enum pgl_mode {
     PGL_MODE_REPLAY = 1
 } pgl_mode;
 
+/* How the Hogwild kernel draws the primary step of each update. */
+typedef enum pgl_sampling {
+    /* The iteration's N = 10*S/srf picks are enumerated, q in [0, N), step
+     * q mod S: every step is the primary endpoint exactly N/S times (without
+     * replacement); 32 consecutive picks form one warp round whose step
+     * records are one coalesced load and whose in-tile partners are shared
+     * by __shfl_sync. Partner, coins and update as the reference. */
+    PGL_SAMPLING_TILES = 0,
+    /* weighted_step_select per pick, i.i.d. (graph.hpp:123-138). */
+    PGL_SAMPLING_IID = 1
+} pgl_sampling;
+
 typedef enum pgl_coord_precision {
     PGL_COORD_F32 = 0, /* one float4 {sx,sy,ex,ey} per node (16 B)   */
     PGL_COORD_F64 = 1  /* two double2 per node (32 B = one sector)  */
@@ -125,7 +137,8 @@ typedef struct pgl_layout_ext {
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
     uint32_t kernel_variant;  /* 0 = 2 CTAs/SM, no spills; 1 = 3 CTAs/SM (80 regs) */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
-    uint32_t _reserved[8];
+    uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */
+    uint32_t _reserved[7];
 } pgl_layout_ext;
 
 void pgl_layout_ext_default(pgl_layout_ext* ext);

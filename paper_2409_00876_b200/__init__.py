@@ -34,7 +34,7 @@ __all__ = [
     "Timing", "run_layout", "run_layout_reuse", "sampled_path_stress", "make_schedule",
     "init_layout", "build_graph", "generate_synthetic_pangenome", "layout_shards",
     "device_count", "Error", "MODE_HOGWILD", "MODE_REPLAY", "COORD_F32", "COORD_F64",
-    "SPS_COUNTER", "SPS_STREAM", "LIB_PATH",
+    "SPS_COUNTER", "SPS_STREAM", "SAMPLING_TILES", "SAMPLING_IID", "LIB_PATH",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -51,6 +51,7 @@ _lib = C.CDLL(LIB_PATH)
 MODE_HOGWILD, MODE_REPLAY = 0, 1
 COORD_F32, COORD_F64 = 0, 1
 SPS_COUNTER, SPS_STREAM = 0, 1
+SAMPLING_TILES, SAMPLING_IID = 0, 1
 
 _u64p = C.POINTER(C.c_uint64)
 _f64p = C.POINTER(C.c_double)
@@ -69,7 +70,7 @@ class _Ext(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("mode", C.c_uint32), ("coord_precision", C.c_uint32),
                 ("max_warps", C.c_uint32), ("block_threads", C.c_uint32), ("l2_persist", C.c_uint32),
                 ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
-                ("_reserved", C.c_uint32 * 8)]
+                ("sampling", C.c_uint32), ("_reserved", C.c_uint32 * 7)]
 
 
 class _PathStep(C.Structure):
@@ -229,6 +230,7 @@ class LayoutExt:
     l2_persist: int = 0
     l2_fetch_bytes: int = 0
     kernel_variant: int = 0
+    sampling: int = 0  # SAMPLING_TILES
 
     def _c(self) -> _Ext:
         e = _Ext()
@@ -237,6 +239,7 @@ class LayoutExt:
         e.max_warps, e.block_threads, e.l2_persist = self.max_warps, self.block_threads, self.l2_persist
         e.l2_fetch_bytes = self.l2_fetch_bytes
         e.kernel_variant = self.kernel_variant
+        e.sampling = self.sampling
         return e
 
 

@@ -335,4 +335,38 @@ __device__ __forceinline__ uint64_t zipf_alias(const ZipfAlias* tab, uint32_t zn
     return 1 + (static_cast<uint32_t>(x) < e.x ? col : e.y);
 }
 
+// apply_endpoint_update (engine.cpp:276-306) on the Hogwild store, without
+// calls into IEEE slow paths. Returns 1 if applied.
+template <typename T>
+__device__ __forceinline__ uint32_t hog_update_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                               double d_ref, double eta, Xo& r, uint64_t pol) {
+    if (!(d_ref > 0.0)) return 0;
+    double mu = eta * rcp_nr(d_ref * d_ref);
+    if (mu > 1.0) mu = 1.0;
+    double vix, viy, vjx, vjy;
+    CoordHint<T>::get(coords, ni, ei, pol, vix, viy);
+    CoordHint<T>::get(coords, nj, ej, pol, vjx, vjy);
+    const double dx = vix - vjx;
+    const double dy = viy - vjy;
+    const double s2 = dx * dx + dy * dy;
+    double ux, uy, mag;
+    if (s2 < 1e-18) {  // |v_i - v_j| < 1e-9: random unit direction
+        float sn, cs;
+        sincospif(2.0f * static_cast<float>(r.uniform()), &sn, &cs);
+        ux = cs;
+        uy = sn;
+        mag = sqrt(s2);
+    } else {
+        const double rs = rsqrt_nr(s2);
+        mag = s2 * rs;
+        ux = dx * rs;
+        uy = dy * rs;
+    }
+    const double delta = mu * (mag - d_ref) * 0.5;
+    CoordHint<T>::set(coords, ni, ei, pol, vix - delta * ux, viy - delta * uy);
+    CoordHint<T>::set(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy);
+    return 1;
+}
+
+
 }  // namespace pgl

@@ -325,6 +325,8 @@ struct pgl_graph {
     DevBuf<StepRec> step;
     DevBuf<uint64_t> cum;
     DevBuf<uint32_t> guide;
+    DevBuf<uint32_t> sguide;
+    uint32_t sguide_bits = 0, sguide_shift = 0;
     DevBuf<PathConst> pc;
     DevBuf<ZipfAlias> zalias;
     uint32_t guide_bits = 8;
@@ -351,6 +353,9 @@ struct pgl_graph {
         d.guide = guide.p;
         d.pc = pc.p;
         d.zalias = zalias.p;
+        d.sguide = sguide.p;
+        d.sguide_bits = sguide_bits;
+        d.sguide_shift = sguide_shift;
         d.total_steps = sum.total_steps;
         d.n_paths = n_paths;
         d.guide_bits = guide_bits;
@@ -387,6 +392,23 @@ void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
         const uint64_t first = static_cast<uint64_t>((static_cast<unsigned __int128>(b) * S) >> bits);
         guide[b] = static_cast<uint32_t>(std::upper_bound(cum.begin(), cum.end(), first) - cum.begin() - 1);
         if (guide[b] >= P) guide[b] = P ? P - 1 : 0;
+    }
+    {   // step-index guide: path containing step b << shift (path_of_step)
+        uint32_t L = 1;
+        while ((1ULL << L) < std::max<uint64_t>(S, 2)) ++L;
+        const uint32_t sb = std::min<uint32_t>(L, 14);
+        G->sguide_bits = sb;
+        G->sguide_shift = L - sb;
+        std::vector<uint32_t> sg(1u << sb, 0);
+        for (uint64_t b = 0; b < sg.size(); ++b) {
+            const uint64_t first = b << G->sguide_shift;
+            const uint64_t pth = static_cast<uint64_t>(std::upper_bound(cum.begin(), cum.end(), first) - cum.begin() - 1);
+            sg[b] = static_cast<uint32_t>(std::min<uint64_t>(pth, P ? P - 1 : 0));
+        }
+        G->sguide.alloc(sg.size());
+        PGL_CUDA(cudaMemcpyAsync(G->sguide.p, sg.data(), sg.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                 G->stream));
+        PGL_CUDA(cudaStreamSynchronize(G->stream));
     }
     G->guide.alloc(guide.size());
     PGL_CUDA(cudaMemcpyAsync(G->guide.p, guide.data(), guide.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
@@ -458,9 +480,11 @@ pgl_graph_view view_of(const pgl_graph* G) {
 uint32_t auto_max_warps(uint64_t n_nodes) {
     // Hogwild concurrency cap: keep the number of in-flight updates well
     // below the number of endpoints so concurrent read-modify-writes on one
-    // endpoint stay rare (SURVEY.md §7 hard part 1). One warp per 64 nodes,
-    // at least 4 warps.
-    const uint64_t w = n_nodes / 64;
+    // endpoint stay rare (SURVEY.md §7 hard part 1). One warp (32 lanes) per
+    // 160 nodes, at least 4 warps: config 1 (10k nodes) runs 62 warps, whose
+    // SPS matched the reference within 0.2% in the cap sweep; from ~400k
+    // nodes up the occupancy limit binds first.
+    const uint64_t w = n_nodes / 160;
     return static_cast<uint32_t>(std::max<uint64_t>(4, std::min<uint64_t>(w, 1u << 24)));
 }
 
@@ -485,6 +509,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (G->n_paths == 0 || !G->sum.usable)
         raise(PGL_ERR_DEGENERATE_GRAPH, "layout needs at least one path with two or more steps");
     if (ext.mode != PGL_MODE_HOGWILD && ext.mode != PGL_MODE_REPLAY) raise(PGL_ERR_INVALID_PARAMETER, "unknown mode");
+    if (ext.sampling > PGL_SAMPLING_IID) raise(PGL_ERR_INVALID_PARAMETER, "unknown sampling");
     if (ext.coord_precision > 1) raise(PGL_ERR_INVALID_PARAMETER, "unknown coord_precision");
 
     DeviceGuard dg(G->device);
@@ -561,7 +586,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     uint64_t lanes = 1;
     if (!replay) {
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
-        shape = sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant));
+        shape = ext.sampling == PGL_SAMPLING_IID
+                    ? sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
+                    : tiles_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant));
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -605,7 +632,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     for (auto& e : ev) PGL_CUDA(cudaEventCreate(&e));
     std::vector<double> host_coords;
     bool aborted = false;
+    uint32_t iters_run = 0;
     for (uint32_t it = 0; it < cfg.n_iters && !aborted; ++it) {
+        ++iters_run;
         const double t_it = now_s();
         IterArgs a;
         a.eta = etas[it];
@@ -615,11 +644,26 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         a.batch = cfg.batch_size;
         a.drf = cfg.drf;
         a.n_warps = n_warps;
+        a.units = (spi + 31) / 32;
+        {   // unit order of k_sgd_tiles: u = (a*k + b) mod U, gcd(a, U) = 1,
+            // a near U/phi (low-discrepancy), jittered per iteration
+            HostRng pr(cfg.global_seed, (1ULL << 59) + it);
+            const uint64_t U = std::max<uint64_t>(a.units, 1);
+            uint64_t m = static_cast<uint64_t>(static_cast<double>(U) * 0.6180339887498949) + pr.below(U / 16 + 1);
+            m %= U;
+            if (m == 0) m = 1;
+            while (std::gcd(m, U) != 1) m = (m + 1) % U == 0 ? 1 : m + 1;
+            a.perm_a = m;
+            a.perm_b = pr.below(U);
+            a.perm_step = static_cast<uint64_t>((static_cast<unsigned __int128>(m) * n_warps) % U);
+        }
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
         if (replay)
             launch_sgd_replay(dg_, G->coords64.p, G->rng.p, dstats, a, G->stream);
-        else
+        else if (ext.sampling == PGL_SAMPLING_IID)
             launch_sgd_hogwild(dg_, coords, f64, rng, dstats, a, shape, G->stream);
+        else
+            launch_sgd_tiles(dg_, coords, f64, rng, dstats, a, shape, G->stream);
         PGL_CUDA(cudaEventRecord(ev[2 * it + 1], G->stream));
         if (cb) {  // IterationCallback at the boundary (engine.cpp:223-229)
             const double* cptr = nullptr;
@@ -646,12 +690,11 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     }
     double kms = 0.0;
     uint32_t launches = 0;
-    for (uint32_t it = 0; it < cfg.n_iters; ++it) {
+    for (uint32_t it = 0; it < iters_run; ++it) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]) == cudaSuccess) {
-            kms += ms;
-            ++launches;
-        }
+        PGL_CUDA(cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]));
+        kms += ms;
+        ++launches;
     }
     for (auto& e : ev) cudaEventDestroy(e);
     if (!replay && prev_gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, prev_gran);

@@ -67,6 +67,9 @@ struct DevGraph {
     uint32_t n_paths;
     uint32_t guide_bits;
     uint64_t n_nodes;
+    const uint32_t* sguide;   // [1 << sguide_bits] path of step (b << sguide_shift)
+    uint32_t sguide_shift;
+    uint32_t sguide_bits;
 };
 
 struct IterArgs {
@@ -77,6 +80,12 @@ struct IterArgs {
     uint32_t batch;
     uint32_t drf;
     uint32_t n_warps;     // Hogwild workers = resident warps
+    // tile sampling (k_sgd_tiles): units of 32 consecutive picks q, step
+    // i = q mod S, visited in the order u = (a*k + b) mod U.
+    uint64_t units;       // U = ceil(steps / 32)
+    uint64_t perm_a;      // multiplier, gcd(a, U) = 1, a < U
+    uint64_t perm_b;      // offset < U
+    uint64_t perm_step;   // (a * n_warps) mod U
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].
@@ -107,6 +116,9 @@ void launch_seed_rng(DevRng rng, uint64_t n_lanes, uint64_t seed, void* stream);
 void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng rng,
                         DevStats* stats, const IterArgs& a, LaunchShape shape,
                         void* stream);
+void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_f64, DevRng rng,
+                      DevStats* stats, const IterArgs& a, LaunchShape shape, void* stream);
+LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant);
 void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4,
                        DevStats* stats, const IterArgs& a, void* stream);
 

@@ -115,46 +115,13 @@ __device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const Iter
     return out;
 }
 
-// apply_endpoint_update (engine.cpp:276-306) on the Hogwild store, without
-// calls into IEEE slow paths. Returns 1 if applied.
-template <typename T>
-__device__ __forceinline__ uint32_t hog_update(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                               double d_ref, double eta, Xo& r, uint64_t pol) {
-    if (!(d_ref > 0.0)) return 0;
-    double mu = eta * rcp_nr(d_ref * d_ref);
-    if (mu > 1.0) mu = 1.0;
-    double vix, viy, vjx, vjy;
-    CoordHint<T>::get(coords, ni, ei, pol, vix, viy);
-    CoordHint<T>::get(coords, nj, ej, pol, vjx, vjy);
-    const double dx = vix - vjx;
-    const double dy = viy - vjy;
-    const double s2 = dx * dx + dy * dy;
-    double ux, uy, mag;
-    if (s2 < 1e-18) {  // |v_i - v_j| < 1e-9: random unit direction
-        float sn, cs;
-        sincospif(2.0f * static_cast<float>(r.uniform()), &sn, &cs);
-        ux = cs;
-        uy = sn;
-        mag = sqrt(s2);
-    } else {
-        const double rs = rsqrt_nr(s2);
-        mag = s2 * rs;
-        ux = dx * rs;
-        uy = dy * rs;
-    }
-    const double delta = mu * (mag - d_ref) * 0.5;
-    CoordHint<T>::set(coords, ni, ei, pol, vix - delta * ux, viy - delta * uy);
-    CoordHint<T>::set(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy);
-    return 1;
-}
-
 // Stage B: the update(s) of one selected pair (engine.cpp:133-170).
 template <typename T>
 __device__ __forceinline__ uint32_t stage_update(const Sel& sel, void* coords, Xo& r, const IterArgs& a,
                                                  uint64_t pol) {
     if (!(sel.flags & 1u)) return 0;
     const int ei = (sel.flags >> 1) & 1, ej = (sel.flags >> 2) & 1;
-    uint32_t applied = hog_update<T>(coords, sel.ri.node, ei, sel.rj.node, ej,
+    uint32_t applied = hog_update_t<T>(coords, sel.ri.node, ei, sel.rj.node, ej,
                                      abs_diff(step_pos(sel.ri, ei), step_pos(sel.rj, ej)), a.eta, r, pol);
     if (a.drf > 1) {
         unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
@@ -166,7 +133,7 @@ __device__ __forceinline__ uint32_t stage_update(const Sel& sel, void* coords, X
                 eb = ((bits >> 62) & 1) ? 0 : 1;
             } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
             used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-            applied += hog_update<T>(coords, sel.ri.node, ea, sel.rj.node, eb,
+            applied += hog_update_t<T>(coords, sel.ri.node, ea, sel.rj.node, eb,
                                      abs_diff(step_pos(sel.ri, ea), step_pos(sel.rj, eb)), a.eta, r, pol);
         }
     }

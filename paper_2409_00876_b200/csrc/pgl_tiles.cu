@@ -1,0 +1,242 @@
+// pgl_tiles.cu — tile-sampled Hogwild PG-SGD (the default fast path).
+//
+// Same update as the reference's worker loop (engine.cpp:103-172): per primary
+// step a node i, a partner j on i's path (uniform with one redraw, or a
+// Zipf-distributed hop under cooling, select_step_pair :52-80), coin-flipped
+// endpoints, apply_endpoint_update (:276-306), drf re-updates (:147-170).
+//
+// What changes is how the primary step i is drawn. The reference draws it
+// i.i.d. uniform over all steps (weighted_step_select, graph.hpp:123-138),
+// i.e. 10/srf picks per step per iteration on average. Here the iteration's
+// N = 10*S/srf picks are enumerated, q in [0, N), with i = q mod S: every step
+// is the primary endpoint exactly 10/srf times (sampling without
+// replacement; the marginal of each update is unchanged). Picks are grouped
+// in units of 32 consecutive q, one unit per warp round:
+//   * the 32 step records of a unit are one coalesced 512-byte load (four
+//     full lines) instead of 32 random 16-byte gathers, each of which costs a
+//     whole 128-byte line on B200 (L2 promotes every random miss);
+//   * a partner j that falls inside the unit's 32 steps (most Zipf hops in
+//     the cooling phase) is taken from the owning lane with __shfl_sync, so
+//     lanes working on the same path share step loads;
+//   * the cooling decision of a batch of 32 steps is warp-uniform.
+// Units are visited in the order u = (a*k + b) mod U with gcd(a, U) = 1 and a
+// fresh (a, b) per iteration, warp w taking k = w, w + W, ..., so the warps
+// running at any moment are spread over the whole graph.
+#include <cuda_runtime.h>
+
+#include "pgl_device.cuh"
+
+namespace pgl {
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void flush_stat(DevStats* st, int idx, uint32_t v) {
+    const uint32_t sum = __reduce_add_sync(kFull, v);
+    if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&st->v[idx], static_cast<unsigned long long>(sum));
+}
+
+// Path of global step index i: guide by the step index's high bits, then a
+// short forward scan of cum_steps.
+__device__ __forceinline__ uint32_t path_of_step(const DevGraph& g, uint64_t i) {
+    uint32_t p = __ldg(g.sguide + (i >> g.sguide_shift));
+    while (__ldg(g.cum + p + 1) <= i) ++p;
+    return p;
+}
+
+// Stage A product for one lane: its step i (record in flight), its partner j
+// (record in flight when outside the unit) and the coins.
+struct TileSel {
+    StepRec ri, rj;       // rj valid when !(flags & 8)
+    uint32_t src;         // lane holding j's record when in-tile
+    uint32_t flags;       // bit0 valid, bit1 e_i end, bit2 e_j end, bit3 j in tile
+};
+
+template <typename T, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void* __restrict__ coords, DevRng rng,
+                                                                DevStats* stats, IterArgs a) {
+    const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint32_t warp = static_cast<uint32_t>(tid >> 5);
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= a.n_warps) return;
+
+    Xo r{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t S = g.total_steps;
+    const uint64_t U = a.units;
+    const uint64_t n_mine = warp < U ? (U - warp + a.n_warps - 1) / a.n_warps : 0;  // k = w + m*W < U
+    uint64_t u = warp < U ? (a.perm_a * static_cast<uint64_t>(warp) + a.perm_b) % U : 0;
+
+    uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
+    bool carry = false;
+    uint64_t s_local = 0;  // this warp's step counter for batch boundaries
+
+    // Stage A: batch decision, i's record (coalesced), partner selection.
+    auto select = [&](uint64_t unit) -> TileSel {
+        TileSel o;
+        o.flags = 0;
+        o.src = 0;
+        o.ri = o.rj = StepRec{0, 0, 0, 0};
+        const uint64_t q0 = unit * 32;
+        const uint64_t q = q0 + lane;
+        const bool active = q < a.steps;
+        // batch boundaries count this warp's own steps (engine.cpp:115-124)
+        const uint64_t s = s_local + lane;
+        const uint64_t in_batch = s % a.batch;
+        bool mine = false;
+        if (active && in_batch == 0) {
+            if (a.force_cooling) {
+                mine = true;
+                ++b_second;
+            } else {
+                mine = r.coin();
+                ++b_first;
+                b_first_cool += mine;
+            }
+        }
+        const int opener = in_batch <= lane ? static_cast<int>(lane - in_batch) : -1;
+        const bool opened = __shfl_sync(kFull, mine, opener < 0 ? 0 : opener);
+        const bool cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
+        const uint32_t n_active = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
+        carry = __shfl_sync(kFull, cooling, n_active - 1);  // batch still open after this unit
+        s_local += n_active;
+
+        // every lane loads its record, active or not: an in-tile partner of an
+        // active lane may sit in an inactive lane of the last, partial unit
+        const uint64_t i0 = q0 % S;            // first step of the unit (warp-uniform)
+        uint64_t gi = i0 + lane;
+        if (gi >= S) gi -= S;                  // the unit wraps at the end of a pass
+        o.ri = load_step_stream(g.step + gi, pol_stream);
+        if (!active) return o;
+        const uint32_t p = path_of_step(g, gi);
+        const uint64_t pbase = __ldg(g.cum + p);
+        const int64_t n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
+        if (n < 2) return o;
+        const int64_t i = static_cast<int64_t>(gi - pbase);
+        int64_t j;
+        uint64_t bits;
+        if (cooling) {
+            const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
+            const uint64_t zt = __ldg(&g.pc[p].ztab);
+            const int64_t k = static_cast<int64_t>(zipf_alias(g.zalias + zt, zn, r.next()));
+            bits = r.next();
+            const int64_t sign = (bits >> 61) & 1 ? 1 : -1;
+            j = i + sign * k;
+            if (j < 0 || j >= n) {
+                j = i - sign * k;
+                if (j < 0 || j >= n) {
+                    j = i + sign * k;
+                    j = j < 0 ? 0 : (j > n - 1 ? n - 1 : j);
+                }
+            }
+            if (j == i) return o;
+        } else {
+            j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+            if (j == i) {
+                j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+                if (j == i) return o;
+            }
+            bits = r.next();
+        }
+        const uint64_t gj = pbase + static_cast<uint64_t>(j);
+        uint32_t fl = 1u | ((bits >> 63) ? 0u : 2u) | (((bits >> 62) & 1) ? 0u : 4u);
+        if (gj >= i0 && gj - i0 < 32) {
+            fl |= 8u;
+            o.src = static_cast<uint32_t>(gj - i0);
+        } else {
+            o.rj = load_step_stream(g.step + gj, pol_stream);
+        }
+        o.flags = fl;
+        return o;
+    };
+
+    // Stage B: share in-tile partner records, then the update(s).
+    auto update = [&](TileSel& o) -> uint32_t {
+        StepRec sh;
+        sh.node = __shfl_sync(kFull, o.ri.node, o.src);
+        sh.ps_lo = __shfl_sync(kFull, o.ri.ps_lo, o.src);
+        sh.pe_lo = __shfl_sync(kFull, o.ri.pe_lo, o.src);
+        sh.hi = __shfl_sync(kFull, o.ri.hi, o.src);
+        if (!(o.flags & 1u)) return 0;
+        const StepRec rj = (o.flags & 8u) ? sh : o.rj;
+        const int ei = (o.flags >> 1) & 1, ej = (o.flags >> 2) & 1;
+        uint32_t got = hog_update_t<T>(coords, o.ri.node, ei, rj.node, ej,
+                                       abs_diff(step_pos(o.ri, ei), step_pos(rj, ej)), a.eta, r, pol_keep);
+        if (a.drf > 1) {
+            unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+            for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                int ea, eb;
+                do {
+                    const uint64_t b2 = r.next();
+                    ea = (b2 >> 63) ? 0 : 1;
+                    eb = ((b2 >> 62) & 1) ? 0 : 1;
+                } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                got += hog_update_t<T>(coords, o.ri.node, ea, rj.node, eb,
+                                       abs_diff(step_pos(o.ri, ea), step_pos(rj, eb)), a.eta, r, pol_keep);
+            }
+        }
+        return got;
+    };
+
+    if (n_mine) {
+        TileSel cur = select(u);
+        for (uint64_t m = 0; m < n_mine; ++m) {
+            TileSel nxt;
+            nxt.flags = 0;
+            nxt.src = 0;
+            if (m + 1 < n_mine) {
+                u += a.perm_step;
+                if (u >= U) u -= U;
+                nxt = select(u);
+            }
+            applied += update(cur);
+            cur = nxt;
+        }
+    }
+
+    rng.s0[tid] = r.a;
+    rng.s1[tid] = r.b;
+    rng.s2[tid] = r.c;
+    rng.s3[tid] = r.d;
+    flush_stat(stats, 2, applied);
+    flush_stat(stats, 4, b_first);
+    flush_stat(stats, 5, b_first_cool);
+    flush_stat(stats, 6, b_second);
+    flush_stat(stats, 7, b_second);
+}
+
+template <typename T>
+const void* tiles_fn(int variant) {
+    return variant == 1 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3>)
+                        : reinterpret_cast<const void*>(k_sgd_tiles<T, 1>);
+}
+
+}  // namespace
+
+LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant) {
+    LaunchShape sh;
+    sh.threads = block_threads > 0 ? block_threads : 256;
+    sh.variant = variant;
+    int sms = 0, occ = 0;
+    PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, coord_f64 ? tiles_fn<double>(variant) : tiles_fn<float>(variant), sh.threads, 0));
+    if (occ < 1) occ = 1;
+    uint64_t warps = static_cast<uint64_t>(sms) * occ * (sh.threads / 32);
+    if (max_warps && warps > max_warps) warps = max_warps;
+    if (warps < 1) warps = 1;
+    sh.blocks = static_cast<int>((warps * 32 + sh.threads - 1) / sh.threads);
+    return sh;
+}
+
+void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_f64, DevRng rng, DevStats* stats,
+                      const IterArgs& a, LaunchShape shape, void* stream) {
+    void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
+    PGL_CUDA(cudaLaunchKernel(coord_f64 ? tiles_fn<double>(shape.variant) : tiles_fn<float>(shape.variant),
+                              dim3(shape.blocks), dim3(shape.threads), args, 0, static_cast<cudaStream_t>(stream)));
+}
+
+}  // namespace pgl

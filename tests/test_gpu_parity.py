@@ -183,23 +183,28 @@ def test_sps_rejects_zero_budget(pgl, gpu):
 
 # ---- Hogwild engine ---------------------------------------------------------------
 
-@pytest.mark.parametrize("drf,srf", [(1, 1), (1, 2), (2, 2), (4, 4), (2, 1)])
-def test_hogwild_accounting(pgl, gpu, drf, srf):
+SAMPLERS = [0, 1]  # SAMPLING_TILES, SAMPLING_IID
+
+
+@pytest.mark.parametrize("samp", SAMPLERS)
+@pytest.mark.parametrize("drf,srf", [(1, 1), (1, 2), (2, 2), (4, 4), (2, 1), (1, 3)])
+def test_hogwild_accounting(pgl, gpu, drf, srf, samp):
     g = pgl.generate_synthetic_pangenome(12, 50, 2, 0.1)
     budget = 10 * g.total_steps()
     cfg = pgl.LayoutConfig(n_iters=3, drf=drf, srf=srf)
     st = pgl.RunStats()
-    (pgl.run_layout if drf == 1 else pgl.run_layout_reuse)(g, cfg, stats=st)
+    (pgl.run_layout if drf == 1 else pgl.run_layout_reuse)(g, cfg, stats=st, ext=pgl.LayoutExt(sampling=samp))
     assert st.primary_steps == cfg.n_iters * (budget // srf)
     assert st.updates_attempted == st.primary_steps * drf
     assert st.updates_applied + st.updates_skipped == st.updates_attempted
     assert st.updates_applied > 0
 
 
-def test_hogwild_cooling_fractions(pgl, gpu):
+@pytest.mark.parametrize("samp", SAMPLERS)
+def test_hogwild_cooling_fractions(pgl, gpu, samp):
     g = pgl.generate_synthetic_pangenome(13, 500, 2, 0.0)
     st = pgl.RunStats()
-    pgl.run_layout(g, pgl.LayoutConfig(n_iters=30, batch_size=1), stats=st)
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=30, batch_size=1), stats=st, ext=pgl.LayoutExt(sampling=samp))
     spi = 10 * g.total_steps()
     assert st.batches_first_half == 15 * spi
     assert st.batches_second_half == 15 * spi
@@ -207,27 +212,52 @@ def test_hogwild_cooling_fractions(pgl, gpu):
     assert abs(st.batches_first_half_cooling / st.batches_first_half - 0.5) <= 0.01
 
 
+@pytest.mark.parametrize("samp", SAMPLERS)
 @pytest.mark.parametrize("n_iters", [1, 2, 3])
-def test_hogwild_switch_point(pgl, gpu, n_iters):
+def test_hogwild_switch_point(pgl, gpu, n_iters, samp):
     g = pgl.generate_synthetic_pangenome(14, 40, 1, 0.0)
     spi = 10 * g.total_steps()
     st = pgl.RunStats()
-    pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters, batch_size=1), stats=st)
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters, batch_size=1), stats=st, ext=pgl.LayoutExt(sampling=samp))
     assert st.batches_second_half == (n_iters // 2) * spi
     assert st.batches_first_half == n_iters * spi - (n_iters // 2) * spi
 
 
 def test_hogwild_batches_count_per_warp(pgl, gpu):
-    """batch_size 32: every warp's share opens ceil(share/32) batches."""
+    """batch_size 32, i.i.d. sampler: every warp's share opens ceil(share/32) batches."""
     g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
     st = pgl.RunStats()
     with pgl.DeviceGraph(g) as dg:
-        dg.layout(pgl.LayoutConfig(n_iters=2), stats=st)
+        dg.layout(pgl.LayoutConfig(n_iters=2), stats=st, ext=pgl.LayoutExt(sampling=pgl.SAMPLING_IID))
         warps = dg.timing().device_threads // 32
     spi = 10 * g.total_steps()
     share, rem = divmod(spi, warps)
     per_iter = rem * -(-(share + 1) // 32) + (warps - rem) * -(-share // 32)
     assert st.batches_first_half == per_iter and st.batches_second_half == per_iter
+
+
+def test_tiles_batches_per_unit(pgl, gpu):
+    """batch_size 32, tile sampler: one batch per 32-pick unit (+1 after the
+    partial unit)."""
+    g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
+    st = pgl.RunStats()
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=2), stats=st)
+    units = -(-10 * g.total_steps() // 32)
+    assert units <= st.batches_first_half <= units + 1
+    assert units <= st.batches_second_half <= units + 1
+    assert st.batches_second_half_cooling == st.batches_second_half
+
+
+@pytest.mark.parametrize("samp", SAMPLERS)
+@pytest.mark.parametrize("args", [(3, 400, 3, 0.05), (2, 33, 1, 0.0), (5, 30, 3, 0.3)])
+def test_sampler_coverage_on_odd_sizes(pgl, oracle, gpu, samp, args):
+    """Partial final units, units wrapping across the pass boundary, paths
+    shorter than a unit: layouts stay finite and converge."""
+    g, go = both(pgl, oracle, args)
+    out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=3), ext=pgl.LayoutExt(sampling=samp))
+    assert np.isfinite(out).all()
+    init = oracle.sps(go, oracle.init_layout(go, 3), 5).mean
+    assert oracle.sps(go, out, 5).mean < init / 5.0
 
 
 def test_hogwild_converges_and_finite(pgl, oracle, gpu):
@@ -293,7 +323,8 @@ def test_callback_exception_propagates(pgl, gpu):
 
 
 @pytest.mark.slow
-def test_hogwild_sps_parity_config1(pgl, oracle, ref, gpu):
+@pytest.mark.parametrize("samp", SAMPLERS)
+def test_hogwild_sps_parity_config1(pgl, oracle, ref, gpu, samp):
     """North-star gate on config 1: median SPS over layout seeds 101..105
     (metric seed 7, spn 100, the reference estimator for both sides) within
     2% of the reference's threads=1 layouts."""
@@ -301,7 +332,7 @@ def test_hogwild_sps_parity_config1(pgl, oracle, ref, gpu):
     gr = ref.generate(*C1, gfa_roundtrip=True)
     gpu_sps, cpu_sps = [], []
     for seed in range(101, 106):
-        out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=seed))
+        out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=seed), ext=pgl.LayoutExt(sampling=samp))
         gpu_sps.append(ref.sps(gr, out, 7, 100).mean)
         lay, _ = ref.run_layout(gr, make_cfg(global_seed=seed))
         cpu_sps.append(ref.sps(gr, lay, 7, 100).mean)

@@ -46,6 +46,35 @@ if what == "sweep":
                                           kernel_ms=round(tm.kernel_ms, 1), gupd=round(upd / tm.kernel_ms / 1e6, 3),
                                           applied=round(st.updates_applied / st.updates_attempted, 5), sps10=r.mean)), flush=True)
 
+if what == "tiles":
+    t = time.time(); g = P.generate_synthetic_pangenome(1, 968000, 90, 0.05); print("gen C2 %.2fs" % (time.time() - t), flush=True)
+    dg = P.DeviceGraph(g)
+    upd = 30 * 10 * g.total_steps()
+    for samp in (0, 1):
+        for prec in (0, 1):
+            for var in (0, 1):
+                ext = P.LayoutExt(coord_precision=prec, kernel_variant=var, sampling=samp)
+                dg.layout(P.LayoutConfig(n_iters=2), ext=ext, copy_out=False)
+                st = P.RunStats()
+                dg.layout(P.LayoutConfig(), ext=ext, stats=st, copy_out=False)
+                tm = dg.timing()
+                r = dg.stress(7, 10)
+                print(json.dumps(dict(samp=samp, prec=prec, var=var, lanes=tm.device_threads,
+                                      kernel_ms=round(tm.kernel_ms, 1), gupd=round(upd / tm.kernel_ms / 1e6, 3),
+                                      applied=round(st.updates_applied / st.updates_attempted, 5), sps10=r.mean,
+                                      b=(st.batches_first_half, st.batches_first_half_cooling, st.batches_second_half))), flush=True)
+    if R is not None:
+        gr = R.generate(1, 9680, 8, 0.05, gfa_roundtrip=True)
+        g1 = P.generate_synthetic_pangenome(1, 9680, 8, 0.05)
+        cpu = [1.746489852350168e-05, 1.7414899039291445e-05, 1.7464457322393124e-05, 1.7399e-05, 1.7576e-05]
+        for samp in (0, 1):
+            for cap in (0, 32, 128, 512):
+                vals = []
+                for seed in (101, 102, 103, 104, 105):
+                    out = P.run_layout(g1, P.LayoutConfig(global_seed=seed), ext=P.LayoutExt(max_warps=cap, sampling=samp))
+                    vals.append(R.sps(gr, out, 7, 100).mean)
+                print(json.dumps(dict(c1=1, samp=samp, cap=cap, ratio=float(np.median(vals) / np.median(cpu)), vals=vals)), flush=True)
+
 if what in ("all", "c1") and R is not None:
     g = P.generate_synthetic_pangenome(1, 9680, 8, 0.05)
     gr = R.generate(1, 9680, 8, 0.05, gfa_roundtrip=True)
