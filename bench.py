@@ -13,7 +13,7 @@ run_layout of that graph: 30 x 10 x sum|p| = 2.61e10 attempted updates.
   e2e    : updates/s through the C-ABI drop-in pgl_layout_run with HOST
            buffers: pack + H2D of the graph and initial layout, 30 kernels,
            D2H of the coordinates, every step (host wall, synchronised).
-  roofline: k_sgd_hogwild, 192 algorithmic bytes per update (6 random
+  roofline: k_sgd_tiles, 192 algorithmic bytes per update (6 random
            32-byte sectors) x updates per launch / mean
            launch time, against MEASURED_PEAKS.json hbm_gbs.
   cpu_baseline: the reference library itself (oracle/_ref, built from the
@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--coord", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--coord", choices=["f32", "f64"], default="f64")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
@@ -284,7 +284,7 @@ def run_ours(args, dist: Dist):
         tm = dg.timing()
         dev_ms.append(tm.device_ms)
         kern_ms.append(tm.kernel_ms)
-        launches += tm.launches + 2  # 30 SGD + seed_rng + f64->f32 init narrowing
+        launches += tm.launches + 1 + (1 if args.coord == "f32" else 0)  # SGD + seed_rng (+ f64->f32)
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
@@ -341,7 +341,7 @@ def run_ours(args, dist: Dist):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s, "api": "pgl_layout_run (C-ABI) from host PathStep arrays"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgd_hogwild",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgd_tiles",
                          "bytes_per_update": BYTES_PER_UPDATE, "launch_ms": sgd_launch_ms,
                          "peak_source": peak_src},
             "cpu_baseline": cpu,

@@ -122,8 +122,9 @@ typedef enum pgl_sampling {
 } pgl_sampling;
 
 typedef enum pgl_coord_precision {
-    PGL_COORD_F32 = 0, /* one float4 {sx,sy,ex,ey} per node (16 B)   */
-    PGL_COORD_F64 = 1  /* two double2 per node (32 B = one sector)  */
+    PGL_COORD_F32 = 0, /* one float4 {sx,sy,ex,ey} per node (16 B); loses
+                          local precision once coordinates exceed ~1e7 */
+    PGL_COORD_F64 = 1  /* two double2 per node (32 B = one sector); default */
 } pgl_coord_precision;
 
 /* B200-specific knobs kept out of pgl_layout_config so that struct stays

@@ -224,7 +224,7 @@ class LayoutConfig:
 class LayoutExt:
     """B200 knobs outside LayoutConfig (pgl_layout_ext)."""
     mode: int = MODE_HOGWILD
-    coord_precision: int = COORD_F32
+    coord_precision: int = COORD_F64
     max_warps: int = 0
     block_threads: int = 0
     l2_persist: int = 0

@@ -879,7 +879,7 @@ void pgl_layout_ext_default(pgl_layout_ext* e) {
     std::memset(e, 0, sizeof *e);
     e->struct_size = sizeof(pgl_layout_ext);
     e->mode = PGL_MODE_HOGWILD;
-    e->coord_precision = PGL_COORD_F32;
+    e->coord_precision = PGL_COORD_F64;
 }
 
 int pgl_graph_create(int device, const pgl_graph_view* v, pgl_graph** out) {

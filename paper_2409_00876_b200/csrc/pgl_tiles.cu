@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         // active lane may sit in an inactive lane of the last, partial unit
         const uint64_t i0 = q0 % S;            // first step of the unit (warp-uniform)
         uint64_t gi = i0 + lane;
-        if (gi >= S) gi -= S;                  // the unit wraps at the end of a pass
+        while (gi >= S) gi -= S;               // the unit wraps at the end of a pass (S < 32: repeatedly)
         o.ri = load_step_stream(g.step + gi, pol_stream);
         if (!active) return o;
         const uint32_t p = path_of_step(g, gi);

@@ -140,12 +140,13 @@ def test_sps_counter_bit_exact(pgl, oracle, gpu, args, spn):
     assert (got.mean, got.n, got.std_dev, got.ci_low, got.ci_high, got.skipped) == stress_tuple(want)
 
 
-def test_sps_counter_on_resident_f32_layout(pgl, oracle, gpu):
+@pytest.mark.parametrize("prec", [0, 1])
+def test_sps_counter_on_resident_layout(pgl, oracle, gpu, prec):
     g, go = both(pgl, oracle, C1)
     with pgl.DeviceGraph(g) as dg:
-        lay = dg.layout(pgl.LayoutConfig(n_iters=6))
-        got = dg.stress(7, 20)  # reads the float4 layout left on the device
-    # the copied-out layout is the float layout widened to double: same terms
+        lay = dg.layout(pgl.LayoutConfig(n_iters=6), ext=pgl.LayoutExt(coord_precision=prec))
+        got = dg.stress(7, 20)  # reads the float4 / double2 layout left on the device
+    # the copied-out layout is the device layout (widened to double): same terms
     want = oracle.sps_counter(go, lay, 7, 20)
     assert (got.mean, got.n, got.std_dev, got.skipped) == (want.mean, want.n, want.std_dev, want.skipped)
 

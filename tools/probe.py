@@ -75,6 +75,24 @@ if what == "tiles":
                     vals.append(R.sps(gr, out, 7, 100).mean)
                 print(json.dumps(dict(c1=1, samp=samp, cap=cap, ratio=float(np.median(vals) / np.median(cpu)), vals=vals)), flush=True)
 
+if what == "c3":
+    t = time.time(); g = P.generate_synthetic_pangenome(1, 9680000, 90, 0.05); print("gen C3 %.2fs" % (time.time() - t), g.total_steps(), flush=True)
+    t = time.time(); dg = P.DeviceGraph(g); print("create %.2fs" % (time.time() - t), dg.info(), flush=True)
+    upd = 30 * 10 * g.total_steps()
+    for samp in (0, 1):
+        for prec in (0, 1):
+            ext = P.LayoutExt(coord_precision=prec, sampling=samp)
+            st = P.RunStats()
+            dg.layout(P.LayoutConfig(), ext=ext, stats=st, copy_out=False)
+            tm = dg.timing()
+            r, ms = dg.stress(7, 10, return_ms=True)
+            print(json.dumps(dict(samp=samp, prec=prec, lanes=tm.device_threads, kernel_ms=round(tm.kernel_ms, 1),
+                                  gupd=round(upd / tm.kernel_ms / 1e6, 3), device_ms=round(tm.device_ms, 1),
+                                  applied=round(st.updates_applied / st.updates_attempted, 5), sps10=r.mean, sps_ms=ms)), flush=True)
+    del dg
+    t = time.time(); out = P.run_layout(g, P.LayoutConfig()); e2e = time.time() - t
+    print("e2e C3 run_layout %.2fs -> %.3f G upd/s" % (e2e, upd / e2e / 1e9), flush=True)
+
 if what in ("all", "c1") and R is not None:
     g = P.generate_synthetic_pangenome(1, 9680, 8, 0.05)
     gr = R.generate(1, 9680, 8, 0.05, gfa_roundtrip=True)

@@ -6,7 +6,7 @@ import paper_2409_00876_b200 as P
 cfgs = {"c1": (1, 9680, 8, 0.05), "c2": (1, 968000, 90, 0.05), "c3": (1, 9680000, 90, 0.05)}
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-prec = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+prec = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 g = P.generate_synthetic_pangenome(*cfgs[name])
 dg = P.DeviceGraph(g)
 dg.layout(P.LayoutConfig(n_iters=iters), ext=P.LayoutExt(coord_precision=prec), copy_out=False)
