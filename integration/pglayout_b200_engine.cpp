@@ -1,0 +1,257 @@
+// integration/pglayout_b200_engine.cpp — drop-in replacement for the
+// reference's src/engine.cpp (/root/reference/proj/src/engine.cpp).
+//
+// A maintainer adds this file to the pglayout library instead of
+// src/engine.cpp and links libpgl_b200.so; every declaration of
+// include/pglayout/engine.hpp keeps its signature and meaning:
+//   make_eta_schedule, make_schedule         host (engine.hpp:34-44)
+//   apply_endpoint_update, layout_step       host single-step API, the math
+//                                            oracle of the device kernel
+//                                            (engine.hpp:50-59)
+//   run_layout, run_layout_reuse             -> pgl_layout_run on the GPU
+//                                            (engine.hpp:80-88)
+// Determinism contract (engine.hpp:78-79): threads == 1 runs the bit-exact
+// device replay of the reference's single-worker loop; threads > 1 runs the
+// Hogwild kernel (as nondeterministic as the reference's worker pool).
+// PGLAYOUT_B200_MODE=hogwild|replay overrides; PGLAYOUT_B200_DEVICE picks
+// the GPU. Errors are rethrown as the reference's own exception types.
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "pglayout/engine.hpp"
+#include "pgl_b200.h"
+
+namespace pglayout {
+
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+    const std::string msg = pgl_last_error();
+    // strip the "TypeName: " prefix; the reference constructors add it back
+    const std::string detail = msg.find(": ") != std::string::npos ? msg.substr(msg.find(": ") + 2) : msg;
+    switch (pgl_last_error_type()) {
+        case PGL_ERR_INVALID_PARAMETER: throw InvalidParameter(detail);
+        case PGL_ERR_UNKNOWN_NODE: throw UnknownNode(detail);
+        case PGL_ERR_EMPTY_PATH: throw EmptyPath(detail);
+        case PGL_ERR_INDEX_OUT_OF_RANGE: throw IndexOutOfRange(detail);
+        case PGL_ERR_EMPTY_GRAPH: throw EmptyGraph(detail);
+        case PGL_ERR_DEGENERATE_GRAPH: throw DegenerateGraph(detail);
+        case PGL_ERR_ZERO_REFERENCE: throw ZeroReference(detail);
+        default: break;
+    }
+    throw Error(rc == PGL_E_USAGE ? ErrorKind::usage : rc == PGL_E_INPUT ? ErrorKind::input : ErrorKind::internal,
+                msg);
+}
+
+pgl_layout_config to_c(const LayoutConfig& c) {
+    pgl_layout_config o;
+    pgl_layout_config_default(&o);
+    o.global_seed = c.global_seed;
+    o.n_iters = c.n_iters;
+    o.threads = c.threads;
+    o.batch_size = c.batch_size;
+    o.zipf_theta = c.zipf_theta;
+    o.zipf_space_max = c.zipf_space_max;
+    o.eta_min_eps = c.eta_min_eps;
+    o.drf = c.drf;
+    o.srf = c.srf;
+    return o;
+}
+
+static_assert(sizeof(PathStep) == sizeof(pgl_path_step), "PathStep ABI");
+static_assert(offsetof(PathStep, offset) == offsetof(pgl_path_step, offset), "PathStep ABI");
+static_assert(offsetof(PathStep, node_id) == offsetof(pgl_path_step, node_id), "PathStep ABI");
+static_assert(offsetof(PathStep, seq_len) == offsetof(pgl_path_step, seq_len), "PathStep ABI");
+static_assert(offsetof(PathStep, orient) == offsetof(pgl_path_step, orient), "PathStep ABI");
+
+// A zero-copy view of the graph: the library reads the PathStep arrays in place.
+struct View {
+    std::vector<uint64_t> node_len, n_steps, totals;
+    std::vector<const pgl_path_step*> steps;
+    pgl_graph_view v{};
+    explicit View(const PangenomeGraph& g) {
+        node_len.reserve(g.node_count());
+        for (const NodeRecord& n : g.nodes) node_len.push_back(n.seq_len);
+        for (const Path& p : g.paths) {
+            steps.push_back(reinterpret_cast<const pgl_path_step*>(p.steps.data()));
+            n_steps.push_back(p.steps.size());
+            totals.push_back(p.total_len);
+        }
+        v.n_nodes = g.node_count();
+        v.node_len = node_len.data();
+        v.n_paths = static_cast<uint32_t>(g.paths.size());
+        v.path_steps = steps.data();
+        v.path_n_steps = n_steps.data();
+        v.path_total_len = totals.data();
+    }
+};
+
+struct CbCtx {
+    const IterationCallback* cb;
+    Layout* scratch;
+    std::exception_ptr err;
+};
+
+int trampoline(uint32_t iter, const double* coords, double eta, double secs, void* user) {
+    auto* c = static_cast<CbCtx*>(user);
+    try {
+        const std::size_t n = c->scratch->node_count();
+        for (std::size_t k = 0; k < n; ++k) {
+            c->scratch->set(static_cast<NodeId>(k), Endpoint::start, {coords[4 * k], coords[4 * k + 1]});
+            c->scratch->set(static_cast<NodeId>(k), Endpoint::end, {coords[4 * k + 2], coords[4 * k + 3]});
+        }
+        (*c->cb)(iter, *c->scratch, eta, secs);
+        return 0;
+    } catch (...) {
+        c->err = std::current_exception();
+        return 1;
+    }
+}
+
+Layout run(const PangenomeGraph& g, const LayoutConfig& cfg, const IterationCallback& cb, RunStats* stats,
+           int reuse) {
+    const View view(g);
+    const pgl_layout_config c = to_c(cfg);
+    pgl_layout_ext ext;
+    pgl_layout_ext_default(&ext);
+    ext.mode = cfg.threads == 1 ? PGL_MODE_REPLAY : PGL_MODE_HOGWILD;
+    if (const char* m = std::getenv("PGLAYOUT_B200_MODE")) {
+        if (!std::strcmp(m, "hogwild")) ext.mode = PGL_MODE_HOGWILD;
+        if (!std::strcmp(m, "replay")) ext.mode = PGL_MODE_REPLAY;
+    }
+    const int device = std::getenv("PGLAYOUT_B200_DEVICE") ? std::atoi(std::getenv("PGLAYOUT_B200_DEVICE")) : 0;
+    std::vector<double> coords(4 * g.node_count());
+    Layout scratch(g);
+    CbCtx ctx{&cb, &scratch, nullptr};
+    pgl_run_stats st{};
+    const int rc = pgl_layout_run(device, &view.v, &c, &ext, reuse, cb ? trampoline : nullptr, cb ? 1 : 0, &ctx,
+                                  coords.data(), &st);
+    if (ctx.err) std::rethrow_exception(ctx.err);
+    if (rc != PGL_OK) rethrow(rc);
+    Layout out(g);
+    for (std::size_t k = 0; k < g.node_count(); ++k) {
+        out.set(static_cast<NodeId>(k), Endpoint::start, {coords[4 * k], coords[4 * k + 1]});
+        out.set(static_cast<NodeId>(k), Endpoint::end, {coords[4 * k + 2], coords[4 * k + 3]});
+    }
+    if (stats) {
+        stats->primary_steps = st.primary_steps;
+        stats->updates_attempted = st.updates_attempted;
+        stats->updates_applied = st.updates_applied;
+        stats->updates_skipped = st.updates_skipped;
+        stats->batches_first_half = st.batches_first_half;
+        stats->batches_first_half_cooling = st.batches_first_half_cooling;
+        stats->batches_second_half = st.batches_second_half;
+        stats->batches_second_half_cooling = st.batches_second_half_cooling;
+    }
+    return out;
+}
+
+// ---- host single-step API (engine.cpp:52-91, :276-321 semantics) -------------
+
+uint64_t step_position(const Path& p, std::uint64_t k, Endpoint e) { return path_position(p, k, e); }
+
+double ref_distance(const Path& p, std::uint64_t i, Endpoint ei, std::uint64_t j, Endpoint ej) {
+    const uint64_t a = step_position(p, i, ei), b = step_position(p, j, ej);
+    return static_cast<double>(a > b ? a - b : b - a);
+}
+
+Endpoint coin_endpoint(RngState& rng) { return rng.flip_coin() ? Endpoint::start : Endpoint::end; }
+
+}  // namespace
+
+SgdSchedule make_eta_schedule(double eta_max, double eta_min, std::uint32_t n_iters) {
+    if (n_iters < 1) throw InvalidParameter("schedule needs n_iters >= 1");
+    if (!(eta_max > 0.0) || !(eta_min > 0.0) || !(eta_min <= eta_max))
+        throw InvalidParameter("schedule needs 0 < eta_min <= eta_max");
+    SgdSchedule s;
+    s.eta_max = eta_max;
+    s.eta_min = eta_min;
+    s.lambda = n_iters > 1 ? std::log(eta_max / eta_min) / (n_iters - 1) : 0.0;
+    for (std::uint32_t t = 0; t < n_iters; ++t) s.etas.push_back(eta_max * std::exp(-s.lambda * t));
+    return s;
+}
+
+SgdSchedule make_schedule(const PangenomeGraph& g, const LayoutConfig& cfg) {
+    const View view(g);
+    const pgl_layout_config c = to_c(cfg);
+    // the schedule is computed by the same host code the device run uses
+    std::vector<double> etas(std::max<std::uint32_t>(cfg.n_iters, 1));
+    const int rc = pgl_make_schedule(&view.v, &c, etas.data());
+    if (rc != PGL_OK) rethrow(rc);
+    std::uint64_t d_max = 1;
+    for (const Path& p : g.paths) d_max = std::max(d_max, p.total_len);
+    SgdSchedule s;
+    s.etas = std::move(etas);
+    s.eta_max = static_cast<double>(d_max) * static_cast<double>(d_max);
+    s.eta_min = cfg.eta_min_eps;
+    s.lambda = cfg.n_iters > 1 ? std::log(s.eta_max / s.eta_min) / (cfg.n_iters - 1) : 0.0;
+    return s;
+}
+
+StepOutcome apply_endpoint_update(Layout& layout, NodeId node_i, Endpoint e_i, NodeId node_j, Endpoint e_j,
+                                  double d_ref, double eta, RngState& rng) {
+    if (!(d_ref > 0.0)) return StepOutcome::skipped;
+    double mu = eta * (1.0 / (d_ref * d_ref));
+    if (mu > 1.0) mu = 1.0;
+    const Vec2 vi = layout.get(node_i, e_i);
+    const Vec2 vj = layout.get(node_j, e_j);
+    const Vec2 d = vi - vj;
+    const double mag = d.norm();
+    Vec2 u;
+    if (mag < 1e-9) {
+        const double angle = 2.0 * 3.14159265358979323846 * rng.next_uniform();
+        u = {std::cos(angle), std::sin(angle)};
+    } else {
+        u = {d.x / mag, d.y / mag};
+    }
+    const double delta = mu * (mag - d_ref) / 2.0;
+    layout.set(node_i, e_i, {vi.x - delta * u.x, vi.y - delta * u.y});
+    layout.set(node_j, e_j, {vj.x + delta * u.x, vj.y + delta * u.y});
+    return StepOutcome::applied;
+}
+
+StepOutcome layout_step(const PangenomeGraph& g, Layout& layout, RngState& rng, double eta, bool cooling,
+                        const LayoutConfig& cfg) {
+    const StepSelection sel = weighted_step_select(rng, g);
+    const Path& p = g.paths[sel.path_index];
+    const std::int64_t n = static_cast<std::int64_t>(p.steps.size());
+    if (n < 2) return StepOutcome::skipped;
+    const std::int64_t i = static_cast<std::int64_t>(sel.step_index);
+    std::int64_t j;
+    if (cooling) {
+        const std::uint64_t span = static_cast<std::uint64_t>(n - 1);
+        const ZipfSampler z({span < cfg.zipf_space_max ? span : cfg.zipf_space_max, cfg.zipf_theta});
+        const std::int64_t k = static_cast<std::int64_t>(z.sample(rng));
+        const std::int64_t sign = rng.flip_coin() ? 1 : -1;
+        j = i + sign * k;
+        if (j < 0 || j >= n) j = i - sign * k;
+        if (j < 0 || j >= n) j = std::min(std::max<std::int64_t>(i + sign * k, 0), n - 1);
+        if (j == i) return StepOutcome::skipped;
+    } else {
+        j = static_cast<std::int64_t>(rng.next_below(static_cast<std::uint64_t>(n)));
+        if (j == i) j = static_cast<std::int64_t>(rng.next_below(static_cast<std::uint64_t>(n)));
+        if (j == i) return StepOutcome::skipped;
+    }
+    const Endpoint ei = coin_endpoint(rng);
+    const Endpoint ej = coin_endpoint(rng);
+    return apply_endpoint_update(layout, p.steps[i].node_id, ei, p.steps[j].node_id, ej,
+                                 ref_distance(p, i, ei, j, ej), eta, rng);
+}
+
+Layout run_layout(const PangenomeGraph& g, const LayoutConfig& cfg, const IterationCallback& on_iteration,
+                  RunStats* stats) {
+    return run(g, cfg, on_iteration, stats, 0);
+}
+
+Layout run_layout_reuse(const PangenomeGraph& g, const LayoutConfig& cfg, const IterationCallback& on_iteration,
+                        RunStats* stats) {
+    return run(g, cfg, on_iteration, stats, 1);
+}
+
+}  // namespace pglayout
