@@ -149,96 +149,8 @@ template <> struct Coord<double> {
     }
 };
 
-// apply_endpoint_update (engine.cpp:276-306). Both endpoints are read before
-// either is written and i is stored before j, so an aliased pair (a path
-// revisiting a node) resolves exactly as the reference: j's value wins.
-template <typename T>
-__device__ __forceinline__ bool apply_update(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                             double d_ref, double eta, Xo& r) {
-    if (!(d_ref > 0.0)) return false;
-    const double w = 1.0 / (d_ref * d_ref);
-    double mu = eta * w;
-    if (mu > 1.0) mu = 1.0;
-    double vix, viy, vjx, vjy;
-    Coord<T>::get(coords, ni, ei, vix, viy);
-    Coord<T>::get(coords, nj, ej, vjx, vjy);
-    const double dx = vix - vjx;
-    const double dy = viy - vjy;
-    const double mag = sqrt(dx * dx + dy * dy);
-    double ux, uy;
-    if (mag < 1e-9) {
-        const double angle = 2.0 * 3.14159265358979323846 * r.uniform();
-        ux = cos(angle);
-        uy = sin(angle);
-    } else {
-        ux = dx / mag;
-        uy = dy / mag;
-    }
-    const double delta = mu * (mag - d_ref) / 2.0;
-    Coord<T>::set(coords, ni, ei, vix - delta * ux, viy - delta * uy);
-    Coord<T>::set(coords, nj, ej, vjx + delta * ux, vjy + delta * uy);
-    return true;
-}
-
 __device__ __forceinline__ double abs_diff(uint64_t a, uint64_t b) {
     return static_cast<double>(a > b ? a - b : b - a);
-}
-
-// One full step after the batch decision: select_step_pair (engine.cpp:52-80),
-// the endpoint coins (:137-138), the update (:139-145) and the drf>1 extra
-// combinations (:147-170). Returns the number of applied updates; the
-// caller counts drf - applied as skipped.
-template <typename T>
-__device__ __forceinline__ uint32_t pgsgd_step(const DevGraph& g, void* coords, Xo& r,
-                                               bool cooling, double eta, double theta,
-                                               uint32_t drf) {
-    const uint64_t x = r.next();
-    const uint64_t pick = __umul64hi(x, g.total_steps);
-    const uint32_t p = select_path(g, x, pick);
-    const PathConst pc = g.pc[p];
-    const int64_t n = static_cast<int64_t>(pc.n);
-    if (n < 2) return 0;
-    const int64_t i = static_cast<int64_t>(pick - pc.base);
-    int64_t j;
-    if (cooling) {
-        const int64_t k = static_cast<int64_t>(zipf_sample(pc, theta, r));
-        const int64_t sign = r.coin() ? 1 : -1;
-        j = i + sign * k;
-        if (j < 0 || j >= n) {
-            j = i - sign * k;
-            if (j < 0 || j >= n) {
-                j = i + sign * k;
-                j = j < 0 ? 0 : (j > n - 1 ? n - 1 : j);
-            }
-        }
-        if (j == i) return 0;
-    } else {
-        j = static_cast<int64_t>(r.below(pc.n));
-        if (j == i) {
-            j = static_cast<int64_t>(r.below(pc.n));
-            if (j == i) return 0;
-        }
-    }
-    const StepRec ri = load_step(g.step + pc.base + i);
-    const StepRec rj = load_step(g.step + pc.base + j);
-    const int ei = r.coin() ? 0 : 1;  // coin true -> Endpoint::start (engine.cpp:89-91)
-    const int ej = r.coin() ? 0 : 1;
-    uint32_t applied = apply_update<T>(coords, ri.node, ei, rj.node, ej,
-                                       abs_diff(step_pos(ri, ei), step_pos(rj, ej)), eta, r);
-    if (drf > 1) {
-        unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
-        for (uint32_t extra = 1; extra < drf; ++extra) {
-            int a, b;
-            do {
-                a = r.coin() ? 0 : 1;
-                b = r.coin() ? 0 : 1;
-            } while (used & (1u << ((a ? 2 : 0) | (b ? 1 : 0))));
-            used |= 1u << ((a ? 2 : 0) | (b ? 1 : 0));
-            applied += apply_update<T>(coords, ri.node, a, rj.node, b,
-                                       abs_diff(step_pos(ri, a), step_pos(rj, b)), eta, r);
-        }
-    }
-    return applied;
 }
 
 // ---- Hogwild fast path helpers -------------------------------------------------

@@ -11,9 +11,7 @@
 // reference's seed_worker(seed, t) stream; states live in registers for the
 // whole launch and in SoA arrays (coalesced) between launches.
 //
-// k_sgd_replay: one lane runs the reference's threads=1 loop verbatim on
-// FP64 coordinates with seed_worker(seed, 0): bit-identical to
-// pglayout::run_layout(threads = 1).
+// (PGL_MODE_REPLAY lives in pgl_replay.cu.)
 #include <cuda_runtime.h>
 
 #include "pgl_device.cuh"
@@ -180,35 +178,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, voi
     flush_stats(stats, 7, b_second);
 }
 
-__global__ void k_sgd_replay(DevGraph g, double* __restrict__ coords, uint64_t* rng4, DevStats* stats,
-                             IterArgs a) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    Xo r{rng4[0], rng4[1], rng4[2], rng4[3]};
-    unsigned long long applied = 0, bf = 0, bfc = 0, bs = 0;
-    bool cooling = false;
-    for (uint64_t s = 0; s < a.steps; ++s) {
-        if (s % a.batch == 0) {
-            cooling = a.force_cooling || r.coin();
-            if (a.force_cooling)
-                ++bs;
-            else {
-                ++bf;
-                bfc += cooling;
-            }
-        }
-        applied += pgsgd_step<double>(g, coords, r, cooling, a.eta, a.theta, a.drf);
-    }
-    rng4[0] = r.a;
-    rng4[1] = r.b;
-    rng4[2] = r.c;
-    rng4[3] = r.d;
-    stats->v[2] += applied;
-    stats->v[4] += bf;
-    stats->v[5] += bfc;
-    stats->v[6] += bs;
-    stats->v[7] += bs;
-}
-
 __global__ void k_f64_to_f32(const double* __restrict__ s, float* __restrict__ d, uint64_t n) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -259,12 +228,6 @@ void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng r
     void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
     PGL_CUDA(cudaLaunchKernel(coord_f64 ? hogwild_fn<double>(shape.variant) : hogwild_fn<float>(shape.variant),
                               dim3(shape.blocks), dim3(shape.threads), args, 0, s));
-    PGL_CUDA(cudaGetLastError());
-}
-
-void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4, DevStats* stats,
-                       const IterArgs& a, void* stream) {
-    k_sgd_replay<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(g, coords, rng4, stats, a);
     PGL_CUDA(cudaGetLastError());
 }
 
