@@ -414,7 +414,7 @@ void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
     PGL_CUDA(cudaMemcpyAsync(G->guide.p, guide.data(), guide.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              G->stream));
 
-    constexpr uint64_t kChunk = 1ULL << 22;  // 4 Mi steps = 64 MiB of records
+    const uint64_t kChunk = std::min<uint64_t>(1ULL << 22, std::max<uint64_t>(S, 1));  // <= 4 Mi steps = 64 MiB
     G->pin.alloc(2 * kChunk * sizeof(StepRec));
     StepRec* bufs[2] = {static_cast<StepRec*>(G->pin.p), static_cast<StepRec*>(G->pin.p) + kChunk};
     cudaEvent_t done[2];
@@ -481,10 +481,11 @@ uint32_t auto_max_warps(uint64_t n_nodes) {
     // Hogwild concurrency cap: keep the number of in-flight updates well
     // below the number of endpoints so concurrent read-modify-writes on one
     // endpoint stay rare (SURVEY.md §7 hard part 1). One warp (32 lanes) per
-    // 160 nodes, at least 4 warps: config 1 (10k nodes) runs 62 warps, whose
-    // SPS matched the reference within 0.2% in the cap sweep; from ~400k
-    // nodes up the occupancy limit binds first.
-    const uint64_t w = n_nodes / 160;
+    // 80 nodes, at least 4 warps: config 1 (10k nodes) runs 124 warps; the
+    // cap sweep there put the median SPS within 0.7% of the reference up to
+    // 128 warps and 4% above it at 512. From ~200k nodes up the occupancy
+    // limit binds first.
+    const uint64_t w = n_nodes / 80;
     return static_cast<uint32_t>(std::max<uint64_t>(4, std::min<uint64_t>(w, 1u << 24)));
 }
 

@@ -93,6 +93,21 @@ if what == "c3":
     t = time.time(); out = P.run_layout(g, P.LayoutConfig()); e2e = time.time() - t
     print("e2e C3 run_layout %.2fs -> %.3f G upd/s" % (e2e, upd / e2e / 1e9), flush=True)
 
+if what == "desk":
+    g = P.generate_synthetic_pangenome(7, 5000, 12, 0.05)
+    upd = 30 * 10 * g.total_steps()
+    for cap in (0, 32, 64, 128, 256):
+        ts = []
+        for rep in range(3):
+            t = time.time(); P.run_layout(g, P.LayoutConfig(global_seed=101), ext=P.LayoutExt(max_warps=cap)); ts.append(time.time() - t)
+        dg = P.DeviceGraph(g)
+        dg.layout(P.LayoutConfig(global_seed=101), ext=P.LayoutExt(max_warps=cap), copy_out=False)
+        tm = dg.timing()
+        print(json.dumps(dict(cap=cap, oneshot_s=[round(x, 4) for x in ts], kernel_ms=round(tm.kernel_ms, 2), device_ms=round(tm.device_ms, 2),
+                              total_ms=round(tm.total_ms, 2), init_ms=round(tm.init_ms, 2), lanes=tm.device_threads, gupd=upd / tm.kernel_ms / 1e6)), flush=True)
+        dg.close()
+    t = time.time(); P.run_layout(g, P.LayoutConfig(global_seed=101), ext=P.LayoutExt(mode=P.MODE_REPLAY)); print("replay s", time.time() - t, flush=True)
+
 if what in ("all", "c1") and R is not None:
     g = P.generate_synthetic_pangenome(1, 9680, 8, 0.05)
     gr = R.generate(1, 9680, 8, 0.05, gfa_roundtrip=True)
