@@ -121,6 +121,21 @@ typedef enum pgl_sampling {
     PGL_SAMPLING_IID = 1
 } pgl_sampling;
 
+/* Order in which the tile sampler visits its units of 32 picks. Either way
+ * every unit is visited exactly once per iteration; only which units run
+ * concurrently changes. */
+typedef enum pgl_unit_order {
+    PGL_ORDER_AUTO = 0,   /* = PGL_ORDER_FRONTS */
+    /* u = (a*k + b) mod U, a ~ U/phi: concurrent warps spread over the whole
+     * graph (every partner gather is a cold random line). */
+    PGL_ORDER_SPREAD = 1,
+    /* The unit space is cut into F contiguous stretches ("fronts", F prime,
+     * ~front_warps concurrent warps each) swept in parallel, alternating
+     * direction per iteration, rotated by a fresh offset: Zipf partners and
+     * their coordinates fall in the L2-resident trail of their own front. */
+    PGL_ORDER_FRONTS = 2
+} pgl_unit_order;
+
 typedef enum pgl_coord_precision {
     PGL_COORD_F32 = 0, /* one float4 {sx,sy,ex,ey} per node (16 B); loses
                           local precision once coordinates exceed ~1e7 */
@@ -139,7 +154,12 @@ typedef struct pgl_layout_ext {
     uint32_t kernel_variant;  /* 0 = 2 CTAs/SM, no spills; 1 = 3 CTAs/SM (80 regs) */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
     uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */
-    uint32_t _reserved[7];
+    uint32_t unit_order;      /* pgl_unit_order (tile sampling only) */
+    uint32_t front_warps;     /* warps per sweep front (PGL_ORDER_FRONTS); 0 = auto */
+    uint32_t pair_window;     /* uniform partners: 0 = auto (on), 1 = independent draws,
+                                 2 = one shared random window per unit (see pgl_tiles.cu) */
+    uint32_t record_hint;     /* L2 policy of step-record loads: 0 = evict_first, 1 = evict_normal */
+    uint32_t _reserved[3];
 } pgl_layout_ext;
 
 void pgl_layout_ext_default(pgl_layout_ext* ext);

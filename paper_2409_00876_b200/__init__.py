@@ -52,6 +52,7 @@ MODE_HOGWILD, MODE_REPLAY = 0, 1
 COORD_F32, COORD_F64 = 0, 1
 SPS_COUNTER, SPS_STREAM = 0, 1
 SAMPLING_TILES, SAMPLING_IID = 0, 1
+ORDER_AUTO, ORDER_SPREAD, ORDER_FRONTS = 0, 1, 2
 
 _u64p = C.POINTER(C.c_uint64)
 _f64p = C.POINTER(C.c_double)
@@ -70,7 +71,8 @@ class _Ext(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("mode", C.c_uint32), ("coord_precision", C.c_uint32),
                 ("max_warps", C.c_uint32), ("block_threads", C.c_uint32), ("l2_persist", C.c_uint32),
                 ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
-                ("sampling", C.c_uint32), ("_reserved", C.c_uint32 * 7)]
+                ("sampling", C.c_uint32), ("unit_order", C.c_uint32), ("front_warps", C.c_uint32),
+                ("pair_window", C.c_uint32), ("record_hint", C.c_uint32), ("_reserved", C.c_uint32 * 3)]
 
 
 class _PathStep(C.Structure):
@@ -231,6 +233,10 @@ class LayoutExt:
     l2_fetch_bytes: int = 0
     kernel_variant: int = 0
     sampling: int = 0  # SAMPLING_TILES
+    unit_order: int = 0  # ORDER_AUTO
+    front_warps: int = 0
+    pair_window: int = 0  # 0 auto (shared window), 1 independent, 2 shared window
+    record_hint: int = 0  # 0 evict_first, 1 evict_normal
 
     def _c(self) -> _Ext:
         e = _Ext()
@@ -240,6 +246,8 @@ class LayoutExt:
         e.l2_fetch_bytes = self.l2_fetch_bytes
         e.kernel_variant = self.kernel_variant
         e.sampling = self.sampling
+        e.unit_order, e.front_warps = self.unit_order, self.front_warps
+        e.pair_window, e.record_hint = self.pair_window, self.record_hint
         return e
 
 

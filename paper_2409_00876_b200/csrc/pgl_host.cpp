@@ -477,6 +477,21 @@ pgl_graph_view view_of(const pgl_graph* G) {
     return v;
 }
 
+constexpr uint32_t kFrontWarps = 8;  // default concurrent warps per sweep front
+
+uint64_t next_prime(uint64_t n) {
+    if (n <= 2) return 2;
+    for (uint64_t c = n | 1;; c += 2) {
+        bool prime = true;
+        for (uint64_t d = 3; d * d <= c; d += 2)
+            if (c % d == 0) {
+                prime = false;
+                break;
+            }
+        if (prime) return c;
+    }
+}
+
 uint32_t auto_max_warps(uint64_t n_nodes) {
     // Hogwild concurrency cap: keep the number of in-flight updates well
     // below the number of endpoints so concurrent read-modify-writes on one
@@ -657,6 +672,18 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.perm_a = m;
             a.perm_b = pr.below(U);
             a.perm_step = static_cast<uint64_t>((static_cast<unsigned __int128>(m) * n_warps) % U);
+            a.fronts = a.front_len = a.front_rem = 0;
+            a.reverse = it & 1;
+            a.pair_window = ext.pair_window != 1;
+            a.record_hint = ext.record_hint;
+            if (ext.unit_order != PGL_ORDER_SPREAD) {
+                // F prime (so fronts of different passes never sit on the same
+                // step: F does not divide 10/srf) near n_warps / front_warps
+                const uint64_t want = std::max<uint64_t>(1, n_warps / (ext.front_warps ? ext.front_warps : kFrontWarps));
+                a.fronts = std::min<uint64_t>(next_prime(want), U);
+                a.front_len = U / a.fronts;
+                a.front_rem = U % a.fronts;
+            }
         }
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
         if (replay)

@@ -86,6 +86,16 @@ struct IterArgs {
     uint64_t perm_a;      // multiplier, gcd(a, U) = 1, a < U
     uint64_t perm_b;      // offset < U
     uint64_t perm_step;   // (a * n_warps) mod U
+    // fronts order (fronts > 0): k -> front f = k mod F, t = k div F;
+    // u = (start_f + (reverse ? len_f - 1 - t : t) + perm_b) mod U with
+    // len_f = front_len + (f < front_rem), start_f = f*front_len + min(f, front_rem)
+    uint64_t fronts;      // F (0 = spread order)
+    uint64_t front_len;   // U div F
+    uint64_t front_rem;   // U mod F
+    uint32_t reverse;     // sweep direction of this iteration
+    uint32_t pair_window; // uniform partners from one shared random window per unit
+    uint32_t record_hint; // 0 = records evict_first in L2, 1 = evict_normal
+    uint32_t _pad1;
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].

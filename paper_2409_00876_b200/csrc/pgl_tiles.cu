@@ -19,9 +19,13 @@
 //     the cooling phase) is taken from the owning lane with __shfl_sync, so
 //     lanes working on the same path share step loads;
 //   * the cooling decision of a batch of 32 steps is warp-uniform.
-// Units are visited in the order u = (a*k + b) mod U with gcd(a, U) = 1 and a
-// fresh (a, b) per iteration, warp w taking k = w, w + W, ..., so the warps
-// running at any moment are spread over the whole graph.
+// Warp w takes visit indices k = w, w + W, ...; k maps to a unit either
+// (PGL_ORDER_SPREAD) by u = (a*k + b) mod U, gcd(a, U) = 1, fresh (a, b) per
+// iteration, so the warps running at any moment are spread over the whole
+// graph, or (PGL_ORDER_FRONTS, default) by F contiguous stretches of the unit
+// space swept in parallel, ~W/F adjacent units in flight per stretch: the
+// Zipf partners (|j - i| <= 1000) of a front fall in its own L2-resident
+// trail instead of cold random lines.
 #include <cuda_runtime.h>
 
 #include "pgl_device.cuh"
@@ -63,11 +67,21 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 
     Xo r{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
     const uint64_t pol_keep = policy_evict_last();
-    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_stream = a.record_hint ? policy_evict_normal() : policy_evict_first();
     const uint64_t S = g.total_steps;
     const uint64_t U = a.units;
     const uint64_t n_mine = warp < U ? (U - warp + a.n_warps - 1) / a.n_warps : 0;  // k = w + m*W < U
     uint64_t u = warp < U ? (a.perm_a * static_cast<uint64_t>(warp) + a.perm_b) % U : 0;
+    uint64_t k = warp;  // this warp's visit index, k = w + m*W
+    // fronts order: unit of visit index k (see IterArgs)
+    auto front_unit = [&](uint64_t kk) -> uint64_t {
+        const uint64_t f = kk % a.fronts, t = kk / a.fronts;
+        const uint64_t len = a.front_len + (f < a.front_rem ? 1 : 0);
+        const uint64_t start = f * a.front_len + (f < a.front_rem ? f : a.front_rem);
+        const uint64_t uu = start + (a.reverse ? len - 1 - t : t) + a.perm_b;
+        return uu >= U ? uu - U : uu;
+    };
+    if (a.fronts && warp < U) u = front_unit(k);
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
     bool carry = false;
@@ -109,11 +123,25 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         uint64_t gi = i0 + lane;
         while (gi >= S) gi -= S;               // the unit wraps at the end of a pass (S < 32: repeatedly)
         o.ri = load_step_stream(g.step + gi, pol_stream);
-        if (!active) return o;
-        const uint32_t p = path_of_step(g, gi);
-        const uint64_t pbase = __ldg(g.cum + p);
-        const int64_t n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
-        if (n < 2) return o;
+        uint32_t p = 0;
+        uint64_t pbase = 0;
+        int64_t n = 0;
+        if (active) {
+            p = path_of_step(g, gi);
+            pbase = __ldg(g.cum + p);
+            n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
+        }
+        // Shared partner window (uniform batches): lane 0 draws one position
+        // w0 on its path; every uniform lane on that path takes
+        // j = (w0 + (lane ^ m)) mod n. w0 is uniform on [0, n), so each j is
+        // marginally uniform exactly as next_below(|p|) (engine.cpp:70-74);
+        // the 32 partners are 32 consecutive steps (one coalesced record load,
+        // neighbouring coordinates) instead of 32 random lines.
+        uint64_t wx = 0;
+        if (a.pair_window && lane == 0 && active && !cooling && n >= 2) wx = r.next();
+        wx = __shfl_sync(kFull, wx, 0);
+        const uint32_t p0 = __shfl_sync(kFull, p, 0);
+        if (!active || n < 2) return o;
         const int64_t i = static_cast<int64_t>(gi - pbase);
         int64_t j;
         uint64_t bits;
@@ -133,7 +161,14 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             }
             if (j == i) return o;
         } else {
-            j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+            if (wx != 0 && p == p0) {
+                const uint64_t w0 = __umul64hi(wx, static_cast<uint64_t>(n));
+                uint64_t jj = w0 + (lane ^ static_cast<uint32_t>(wx & 31));
+                if (jj >= static_cast<uint64_t>(n)) jj = n >= 32 ? jj - n : jj % n;
+                j = static_cast<int64_t>(jj);
+            } else {
+                j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+            }
             if (j == i) {
                 j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
                 if (j == i) return o;
@@ -188,8 +223,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             nxt.flags = 0;
             nxt.src = 0;
             if (m + 1 < n_mine) {
-                u += a.perm_step;
-                if (u >= U) u -= U;
+                k += a.n_warps;
+                if (a.fronts) {
+                    u = front_unit(k);
+                } else {
+                    u += a.perm_step;
+                    if (u >= U) u -= U;
+                }
                 nxt = select(u);
             }
             applied += update(cur);

@@ -54,8 +54,8 @@ def main():
     t = time.time()
     gr = R.generate(*GEN[args.config])
     g = P.generate_synthetic_pangenome(*GEN[args.config])
-    assert (g.n_nodes(), g.total_steps()) == (gr.n_nodes, gr.total_steps)
-    res = {"config": args.config, "graph": {"nodes": g.n_nodes(), "steps": g.total_steps()},
+    assert (g.n_nodes, g.total_steps()) == (gr.n_nodes, gr.total_steps)
+    res = {"config": args.config, "graph": {"nodes": g.n_nodes, "steps": g.total_steps()},
            "host_threads": args.threads, "metric_seed": 7, "gen_s": round(time.time() - t, 1),
            "gpu": [], "ref": []}
     samp = P.SAMPLING_TILES if args.sampling == "tiles" else P.SAMPLING_IID

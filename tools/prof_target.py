@@ -1,4 +1,6 @@
-"""Short target for ncu: one layout of a config with few iterations."""
+"""Short target for ncu: one layout of a config with few iterations.
+usage: python tools/prof_target.py CONFIG ITERS PREC [ORDER [FRONT_WARPS]]
+ORDER: 0 auto, 1 spread, 2 fronts (pgl_unit_order)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -7,8 +9,11 @@ cfgs = {"c1": (1, 9680, 8, 0.05), "c2": (1, 968000, 90, 0.05), "c3": (1, 9680000
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+order = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+fw = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 g = P.generate_synthetic_pangenome(*cfgs[name])
 dg = P.DeviceGraph(g)
-dg.layout(P.LayoutConfig(n_iters=iters), ext=P.LayoutExt(coord_precision=prec), copy_out=False)
+dg.layout(P.LayoutConfig(n_iters=iters), ext=P.LayoutExt(coord_precision=prec, unit_order=order, front_warps=fw),
+          copy_out=False)
 r = dg.stress(7, 10)
 print("done", dg.timing(), r.mean)
