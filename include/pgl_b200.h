@@ -125,14 +125,15 @@ typedef enum pgl_sampling {
  * every unit is visited exactly once per iteration; only which units run
  * concurrently changes. */
 typedef enum pgl_unit_order {
-    PGL_ORDER_AUTO = 0,   /* = PGL_ORDER_FRONTS */
+    PGL_ORDER_AUTO = 0,   /* = PGL_ORDER_SPREAD (measured: fronts gain nothing once
+                             uniform partners share a window) */
     /* u = (a*k + b) mod U, a ~ U/phi: concurrent warps spread over the whole
      * graph (every partner gather is a cold random line). */
     PGL_ORDER_SPREAD = 1,
     /* The unit space is cut into F contiguous stretches ("fronts", F prime,
      * ~front_warps concurrent warps each) swept in parallel, alternating
-     * direction per iteration, rotated by a fresh offset: Zipf partners and
-     * their coordinates fall in the L2-resident trail of their own front. */
+     * direction per iteration, rotated by a fresh offset, so Zipf partners
+     * fall in the recent trail of their own front. */
     PGL_ORDER_FRONTS = 2
 } pgl_unit_order;
 

@@ -672,11 +672,17 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.perm_a = m;
             a.perm_b = pr.below(U);
             a.perm_step = static_cast<uint64_t>((static_cast<unsigned __int128>(m) * n_warps) % U);
+            {
+                const uint64_t S = G->sum.total_steps;
+                a.i0_step = static_cast<uint64_t>((static_cast<unsigned __int128>(a.perm_step) * 32) % S);
+                const uint64_t uw = static_cast<uint64_t>((static_cast<unsigned __int128>(U) * 32) % S);
+                a.i0_wrap = (a.i0_step + S - uw) % S;
+            }
             a.fronts = a.front_len = a.front_rem = 0;
             a.reverse = it & 1;
             a.pair_window = ext.pair_window != 1;
             a.record_hint = ext.record_hint;
-            if (ext.unit_order != PGL_ORDER_SPREAD) {
+            if (ext.unit_order == PGL_ORDER_FRONTS) {
                 // F prime (so fronts of different passes never sit on the same
                 // step: F does not divide 10/srf) near n_warps / front_warps
                 const uint64_t want = std::max<uint64_t>(1, n_warps / (ext.front_warps ? ext.front_warps : kFrontWarps));

@@ -86,6 +86,8 @@ struct IterArgs {
     uint64_t perm_a;      // multiplier, gcd(a, U) = 1, a < U
     uint64_t perm_b;      // offset < U
     uint64_t perm_step;   // (a * n_warps) mod U
+    uint64_t i0_step;     // (32 * perm_step) mod S: first-step advance of a round
+    uint64_t i0_wrap;     // (32 * (perm_step - U)) mod S: the same when u wraps
     // fronts order (fronts > 0): k -> front f = k mod F, t = k div F;
     // u = (start_f + (reverse ? len_f - 1 - t : t) + perm_b) mod U with
     // len_f = front_len + (f < front_rem), start_f = f*front_len + min(f, front_rem)

@@ -85,10 +85,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
     bool carry = false;
-    uint64_t s_local = 0;  // this warp's step counter for batch boundaries
+    uint32_t b0 = 0;  // this warp's step count mod batch (batch boundaries, engine.cpp:115-124)
 
     // Stage A: batch decision, i's record (coalesced), partner selection.
-    auto select = [&](uint64_t unit) -> TileSel {
+    auto select = [&](uint64_t unit, uint64_t unit_i0) -> TileSel {
         TileSel o;
         o.flags = 0;
         o.src = 0;
@@ -97,8 +97,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const uint64_t q = q0 + lane;
         const bool active = q < a.steps;
         // batch boundaries count this warp's own steps (engine.cpp:115-124)
-        const uint64_t s = s_local + lane;
-        const uint64_t in_batch = s % a.batch;
+        uint32_t in_batch = b0 + lane;
+        if (a.batch >= 32) {
+            if (in_batch >= a.batch) in_batch -= a.batch;
+        } else {
+            in_batch %= a.batch;
+        }
         bool mine = false;
         if (active && in_batch == 0) {
             if (a.force_cooling) {
@@ -115,14 +119,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const bool cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
         const uint32_t n_active = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
         carry = __shfl_sync(kFull, cooling, n_active - 1);  // batch still open after this unit
-        s_local += n_active;
+        b0 = (b0 + n_active) % a.batch;
 
         // every lane loads its record, active or not: an in-tile partner of an
         // active lane may sit in an inactive lane of the last, partial unit
-        const uint64_t i0 = q0 % S;            // first step of the unit (warp-uniform)
+        const uint64_t i0 = unit_i0;           // first step of the unit, q0 mod S (warp-uniform)
         uint64_t gi = i0 + lane;
         while (gi >= S) gi -= S;               // the unit wraps at the end of a pass (S < 32: repeatedly)
-        o.ri = load_step_stream(g.step + gi, pol_stream);
         uint32_t p = 0;
         uint64_t pbase = 0;
         int64_t n = 0;
@@ -141,6 +144,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         if (a.pair_window && lane == 0 && active && !cooling && n >= 2) wx = r.next();
         wx = __shfl_sync(kFull, wx, 0);
         const uint32_t p0 = __shfl_sync(kFull, p, 0);
+        // the unit's records (one coalesced 512-byte load), issued after the
+        // path lookup so its DRAM latency is waited for only in next round's update
+        o.ri = load_step_stream(g.step + gi, pol_stream);
         if (!active || n < 2) return o;
         const int64_t i = static_cast<int64_t>(gi - pbase);
         int64_t j;
@@ -216,8 +222,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         return got;
     };
 
+    // i0 = 32u mod S, kept incrementally in spread order (no 64-bit division
+    // per round): u advances by perm_step, or by perm_step - U on a wrap
+    uint64_t i0 = (u * 32) % S;
     if (n_mine) {
-        TileSel cur = select(u);
+        TileSel cur = select(u, i0);
         for (uint64_t m = 0; m < n_mine; ++m) {
             TileSel nxt;
             nxt.flags = 0;
@@ -226,11 +235,18 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 k += a.n_warps;
                 if (a.fronts) {
                     u = front_unit(k);
+                    i0 = (u * 32) % S;
                 } else {
                     u += a.perm_step;
-                    if (u >= U) u -= U;
+                    if (u >= U) {
+                        u -= U;
+                        i0 += a.i0_wrap;
+                    } else {
+                        i0 += a.i0_step;
+                    }
+                    if (i0 >= S) i0 -= S;
                 }
-                nxt = select(u);
+                nxt = select(u, i0);
             }
             applied += update(cur);
             cur = nxt;

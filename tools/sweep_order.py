@@ -26,7 +26,7 @@ def ext_of(v):
             e.unit_order = P.ORDER_SPREAD
         elif part == "fronts":
             e.unit_order = P.ORDER_FRONTS
-        elif part.startswith("w"):
+        elif part.startswith("w") and part[1:].isdigit():
             e.max_warps = int(part[1:])
         elif part == "nowin":
             e.pair_window = 1
