@@ -152,15 +152,18 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t kernel_variant;  /* 0 = 2 CTAs/SM, no spills; 1 = 3 CTAs/SM (80 regs) */
+    uint32_t kernel_variant;  /* tile kernel: 0 = two-stage pipeline (2 CTAs/SM); 1 = two-stage,
+                                 3 CTAs/SM (80 regs); 2 = four-stage pipeline with L2 prefetch */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
     uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */
     uint32_t unit_order;      /* pgl_unit_order (tile sampling only) */
     uint32_t front_warps;     /* warps per sweep front (PGL_ORDER_FRONTS); 0 = auto */
-    uint32_t pair_window;     /* uniform partners: 0 = auto (on), 1 = independent draws,
-                                 2 = one shared random window per unit (see pgl_tiles.cu) */
+    uint32_t pair_window;     /* 0 = auto (= 3), 1 = independent partner draws,
+                                 2 = one shared random window per unit (see pgl_tiles.cu),
+                                 3 = 2 + one shared Zipf hop per unit in cooling batches */
     uint32_t record_hint;     /* L2 policy of step-record loads: 0 = evict_first, 1 = evict_normal */
-    uint32_t _reserved[3];
+    uint32_t hop_lanes;       /* lanes sharing one Zipf hop (pair_window 3); 0 = auto (8) */
+    uint32_t _reserved[2];
 } pgl_layout_ext;
 
 void pgl_layout_ext_default(pgl_layout_ext* ext);

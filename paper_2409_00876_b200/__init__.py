@@ -72,7 +72,8 @@ class _Ext(C.Structure):
                 ("max_warps", C.c_uint32), ("block_threads", C.c_uint32), ("l2_persist", C.c_uint32),
                 ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
                 ("sampling", C.c_uint32), ("unit_order", C.c_uint32), ("front_warps", C.c_uint32),
-                ("pair_window", C.c_uint32), ("record_hint", C.c_uint32), ("_reserved", C.c_uint32 * 3)]
+                ("pair_window", C.c_uint32), ("record_hint", C.c_uint32), ("hop_lanes", C.c_uint32),
+                ("_reserved", C.c_uint32 * 2)]
 
 
 class _PathStep(C.Structure):
@@ -235,8 +236,9 @@ class LayoutExt:
     sampling: int = 0  # SAMPLING_TILES
     unit_order: int = 0  # ORDER_AUTO
     front_warps: int = 0
-    pair_window: int = 0  # 0 auto (shared window), 1 independent, 2 shared window
+    pair_window: int = 0  # 0 auto (= 3), 1 independent draws, 2 shared uniform window, 3 window + shared Zipf hop
     record_hint: int = 0  # 0 evict_first, 1 evict_normal
+    hop_lanes: int = 0  # lanes per shared Zipf hop (pair_window 3), 0 = auto
 
     def _c(self) -> _Ext:
         e = _Ext()
@@ -247,7 +249,7 @@ class LayoutExt:
         e.kernel_variant = self.kernel_variant
         e.sampling = self.sampling
         e.unit_order, e.front_warps = self.unit_order, self.front_warps
-        e.pair_window, e.record_hint = self.pair_window, self.record_hint
+        e.pair_window, e.record_hint, e.hop_lanes = self.pair_window, self.record_hint, self.hop_lanes
         return e
 
 

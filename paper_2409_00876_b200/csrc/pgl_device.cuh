@@ -252,17 +252,44 @@ __device__ __forceinline__ uint64_t zipf_alias(const ZipfAlias* tab, uint32_t zn
     return 1 + (static_cast<uint32_t>(x) < e.x ? col : e.y);
 }
 
+// L2 prefetches for the pipelined tile kernel: a bulk (TMA-engine) prefetch of
+// a contiguous byte range, and a one-sector prefetch of a coordinate endpoint.
+__device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_keep(const void* p) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(p));
+}
+template <typename T>
+__device__ __forceinline__ const void* coord_addr(const void* base, uint32_t node, int end) {
+    return reinterpret_cast<const char*>(base) + (2 * static_cast<uint64_t>(node) + end) * (2 * sizeof(T));
+}
+
 // apply_endpoint_update (engine.cpp:276-306) on the Hogwild store, without
 // calls into IEEE slow paths. Returns 1 if applied.
+template <typename T>
+__device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                              double d_ref, double eta, Xo& r, uint64_t pol, double vix,
+                                              double viy, double vjx, double vjy);
+
 template <typename T>
 __device__ __forceinline__ uint32_t hog_update_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
                                                double d_ref, double eta, Xo& r, uint64_t pol) {
     if (!(d_ref > 0.0)) return 0;
-    double mu = eta * rcp_nr(d_ref * d_ref);
-    if (mu > 1.0) mu = 1.0;
     double vix, viy, vjx, vjy;
     CoordHint<T>::get(coords, ni, ei, pol, vix, viy);
     CoordHint<T>::get(coords, nj, ej, pol, vjx, vjy);
+    return hog_apply_t<T>(coords, ni, ei, nj, ej, d_ref, eta, r, pol, vix, viy, vjx, vjy);
+}
+
+// The arithmetic and write-back half of hog_update_t, on endpoint values the
+// caller loaded (d_ref > 0).
+template <typename T>
+__device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                              double d_ref, double eta, Xo& r, uint64_t pol, double vix,
+                                              double viy, double vjx, double vjy) {
+    double mu = eta * rcp_nr(d_ref * d_ref);
+    if (mu > 1.0) mu = 1.0;
     const double dx = vix - vjx;
     const double dy = viy - vjy;
     const double s2 = dx * dx + dy * dy;

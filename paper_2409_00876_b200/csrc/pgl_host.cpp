@@ -478,6 +478,7 @@ pgl_graph_view view_of(const pgl_graph* G) {
 }
 
 constexpr uint32_t kFrontWarps = 8;  // default concurrent warps per sweep front
+constexpr uint32_t kHopLanes = 8;    // default lanes per shared Zipf hop
 
 uint64_t next_prime(uint64_t n) {
     if (n <= 2) return 2;
@@ -517,6 +518,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.struct_size mismatch");
         std::memcpy(&ext, extp, extp->struct_size);
     }
+    if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.hop_lanes must be 0 or a power of two <= 32");
     if (reuse) {  // run_layout_reuse, engine.cpp:328-334
         if (cfg.drf != 2 && cfg.drf != 4) raise(PGL_ERR_INVALID_PARAMETER, "update reuse needs drf of 2 or 4");
         if (cfg.srf < 1) raise(PGL_ERR_INVALID_PARAMETER, "srf must be >= 1");
@@ -604,7 +607,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
         shape = ext.sampling == PGL_SAMPLING_IID
                     ? sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
-                    : tiles_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant));
+                    : tiles_shape(G->device, f64, cap, static_cast<int>(ext.block_threads),
+                                  ext.unit_order == PGL_ORDER_FRONTS && ext.kernel_variant == 2
+                                      ? 0 : static_cast<int>(ext.kernel_variant));
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -680,8 +685,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             }
             a.fronts = a.front_len = a.front_rem = 0;
             a.reverse = it & 1;
-            a.pair_window = ext.pair_window != 1;
+            a.pair_window = ext.pair_window == 1 ? 0 : (ext.pair_window == 2 ? 1 : 3);
             a.record_hint = ext.record_hint;
+            a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : kHopLanes;
             if (ext.unit_order == PGL_ORDER_FRONTS) {
                 // F prime (so fronts of different passes never sit on the same
                 // step: F does not divide 10/srf) near n_warps / front_warps

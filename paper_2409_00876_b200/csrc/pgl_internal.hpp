@@ -97,7 +97,7 @@ struct IterArgs {
     uint32_t reverse;     // sweep direction of this iteration
     uint32_t pair_window; // uniform partners from one shared random window per unit
     uint32_t record_hint; // 0 = records evict_first in L2, 1 = evict_normal
-    uint32_t _pad1;
+    uint32_t hop_lanes;   // lanes sharing one Zipf hop (pair_window 3): 1..32, power of two
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].

@@ -57,7 +57,15 @@ struct TileSel {
     uint32_t flags;       // bit0 valid, bit1 e_i end, bit2 e_j end, bit3 j in tile
 };
 
-template <typename T, int kMinBlocks>
+// kDepth 2 (default): select(m+1) overlapped with update(m). kDepth 4
+// (variant 2, spread order only): a four-stage software pipeline per warp,
+// one unit per stage, so every load is issued one round before it is used:
+//   A  unit m+3: bulk L2 prefetch of its 512 record bytes (TMA engine, lane 0)
+//   B  unit m+2: batch coin, path, partner selection; record loads (L2 hits)
+//   C  unit m+1: in-tile partner records by shuffle; L2 prefetch of the two
+//                coordinate endpoints
+//   D  unit m:   endpoint loads (L2 hits), update, write-back
+template <typename T, int kMinBlocks, int kDepth>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                 DevStats* stats, IterArgs a) {
     const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -134,16 +142,32 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             pbase = __ldg(g.cum + p);
             n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
         }
-        // Shared partner window (uniform batches): lane 0 draws one position
-        // w0 on its path; every uniform lane on that path takes
-        // j = (w0 + (lane ^ m)) mod n. w0 is uniform on [0, n), so each j is
-        // marginally uniform exactly as next_below(|p|) (engine.cpp:70-74);
-        // the 32 partners are 32 consecutive steps (one coalesced record load,
-        // neighbouring coordinates) instead of 32 random lines.
-        uint64_t wx = 0;
-        if (a.pair_window && lane == 0 && active && !cooling && n >= 2) wx = r.next();
-        wx = __shfl_sync(kFull, wx, 0);
-        const uint32_t p0 = __shfl_sync(kFull, p, 0);
+        // Shared partner draws. Uniform batches (pair_window >= 1): lane 0
+        // draws one position w0 on its path; every uniform lane on that path
+        // takes j = (w0 + (lane ^ m)) mod n. w0 is uniform on [0, n), so each j
+        // is marginally uniform exactly as next_below(|p|) (engine.cpp:70-74).
+        // Cooling batches (pair_window 3): the first lane of each group of
+        // hop_lanes draws one Zipf hop and one sign for the group's lanes on
+        // its path; each lane's (k, sign) is still Zipf x fair coin
+        // (select_step_pair, engine.cpp:57-69). Either way the partners are
+        // consecutive steps: coalesced record loads and neighbouring
+        // coordinates instead of one random line per lane.
+        // tag: bits 0-28 path, 29 leader was cooling, 30 draw valid, 31 sign
+        uint64_t draw = 0;
+        uint32_t tag = p;
+        {
+            const bool win_lead = lane == 0 && !cooling && a.pair_window != 0;
+            const bool hop_lead = (lane & (a.hop_lanes - 1)) == 0 && cooling && a.pair_window == 3;
+            if (active && n >= 2 && (win_lead || hop_lead)) {
+                draw = r.next();
+                tag |= (1u << 30) | (cooling ? (1u << 29) : 0u);
+                if (cooling) tag |= static_cast<uint32_t>(r.next() >> 63) << 31;
+            }
+        }
+        const int lead = cooling ? static_cast<int>(lane & ~(a.hop_lanes - 1)) : 0;
+        draw = __shfl_sync(kFull, draw, lead);
+        tag = __shfl_sync(kFull, tag, lead);
+        const bool shared = ((tag >> 30) & 1) && ((tag >> 29) & 1) == (cooling ? 1u : 0u) && (tag & 0x1FFFFFFFu) == p;
         // the unit's records (one coalesced 512-byte load), issued after the
         // path lookup so its DRAM latency is waited for only in next round's update
         o.ri = load_step_stream(g.step + gi, pol_stream);
@@ -154,9 +178,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         if (cooling) {
             const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
             const uint64_t zt = __ldg(&g.pc[p].ztab);
-            const int64_t k = static_cast<int64_t>(zipf_alias(g.zalias + zt, zn, r.next()));
+            const int64_t k = static_cast<int64_t>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
             bits = r.next();
-            const int64_t sign = (bits >> 61) & 1 ? 1 : -1;
+            const int64_t sign = (shared ? (tag >> 31) : ((bits >> 61) & 1)) ? 1 : -1;
             j = i + sign * k;
             if (j < 0 || j >= n) {
                 j = i - sign * k;
@@ -167,9 +191,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             }
             if (j == i) return o;
         } else {
-            if (wx != 0 && p == p0) {
-                const uint64_t w0 = __umul64hi(wx, static_cast<uint64_t>(n));
-                uint64_t jj = w0 + (lane ^ static_cast<uint32_t>(wx & 31));
+            if (shared) {
+                const uint64_t w0 = __umul64hi(draw, static_cast<uint64_t>(n));
+                uint64_t jj = w0 + (lane ^ static_cast<uint32_t>(draw & 31));
                 if (jj >= static_cast<uint64_t>(n)) jj = n >= 32 ? jj - n : jj % n;
                 j = static_cast<int64_t>(jj);
             } else {
@@ -225,31 +249,120 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     // i0 = 32u mod S, kept incrementally in spread order (no 64-bit division
     // per round): u advances by perm_step, or by perm_step - U on a wrap
     uint64_t i0 = (u * 32) % S;
-    if (n_mine) {
-        TileSel cur = select(u, i0);
-        for (uint64_t m = 0; m < n_mine; ++m) {
-            TileSel nxt;
-            nxt.flags = 0;
-            nxt.src = 0;
-            if (m + 1 < n_mine) {
-                k += a.n_warps;
-                if (a.fronts) {
-                    u = front_unit(k);
-                    i0 = (u * 32) % S;
-                } else {
-                    u += a.perm_step;
-                    if (u >= U) {
-                        u -= U;
-                        i0 += a.i0_wrap;
+    auto advance = [&](uint64_t& uu, uint64_t& ii) {
+        uu += a.perm_step;
+        if (uu >= U) {
+            uu -= U;
+            ii += a.i0_wrap;
+        } else {
+            ii += a.i0_step;
+        }
+        if (ii >= S) ii -= S;
+    };
+    if (kDepth == 2) {
+        if (n_mine) {
+            TileSel cur = select(u, i0);
+            for (uint64_t m = 0; m < n_mine; ++m) {
+                TileSel nxt;
+                nxt.flags = 0;
+                nxt.src = 0;
+                if (m + 1 < n_mine) {
+                    k += a.n_warps;
+                    if (a.fronts) {
+                        u = front_unit(k);
+                        i0 = (u * 32) % S;
                     } else {
-                        i0 += a.i0_step;
+                        advance(u, i0);
                     }
-                    if (i0 >= S) i0 -= S;
+                    nxt = select(u, i0);
                 }
-                nxt = select(u, i0);
+                applied += update(cur);
+                cur = nxt;
             }
-            applied += update(cur);
+        }
+    } else if (n_mine) {
+        // Stage A: the unit's record bytes into L2 (wrapping at the end of a pass)
+        auto prefetch_unit = [&](uint64_t uu, uint64_t ii) {
+            if (S < 32) return;  // warp-uniform arguments: one UBLKPF per warp
+            const uint64_t q0 = uu * 32;
+            const uint32_t n_act = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
+            const uint32_t first = static_cast<uint32_t>(S - ii < n_act ? S - ii : n_act);
+            prefetch_bulk_l2(g.step + ii, first * static_cast<uint32_t>(sizeof(StepRec)));
+            if (first < n_act) prefetch_bulk_l2(g.step, (n_act - first) * static_cast<uint32_t>(sizeof(StepRec)));
+        };
+        // Stage C: resolve in-tile partners, prefetch both endpoints into L2
+        auto resolve = [&](TileSel& o) {
+            StepRec sh;
+            sh.node = __shfl_sync(kFull, o.ri.node, o.src);
+            sh.ps_lo = __shfl_sync(kFull, o.ri.ps_lo, o.src);
+            sh.pe_lo = __shfl_sync(kFull, o.ri.pe_lo, o.src);
+            sh.hi = __shfl_sync(kFull, o.ri.hi, o.src);
+            if (o.flags & 8u) o.rj = sh;
+            if (o.flags & 1u) {
+                prefetch_l2_keep(coord_addr<T>(coords, o.ri.node, (o.flags >> 1) & 1));
+                prefetch_l2_keep(coord_addr<T>(coords, o.rj.node, (o.flags >> 2) & 1));
+            }
+        };
+        uint64_t pu = u, pi = i0;  // prefetch cursor: one unit ahead of the select cursor
+        prefetch_unit(pu, pi);
+        for (int t = 1; t < 3 && t < static_cast<int>(n_mine); ++t) {
+            advance(pu, pi);
+            prefetch_unit(pu, pi);
+        }
+        TileSel cur = select(u, i0);  // unit 0
+        resolve(cur);
+        TileSel nxt;
+        nxt.flags = 0;
+        nxt.src = 0;
+        if (n_mine > 1) {
+            advance(u, i0);
+            nxt = select(u, i0);      // unit 1
+        }
+        for (uint64_t m = 0; m < n_mine; ++m) {
+            if (m + 3 < n_mine) {
+                advance(pu, pi);
+                prefetch_unit(pu, pi);
+            }
+            // Stage D loads for unit m
+            const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
+            double d_ref = 0.0;
+            double vix = 0, viy = 0, vjx = 0, vjy = 0;
+            if (cur.flags & 1u) {
+                d_ref = abs_diff(step_pos(cur.ri, ei), step_pos(cur.rj, ej));
+                if (d_ref > 0.0) {
+                    CoordHint<T>::get(coords, cur.ri.node, ei, pol_keep, vix, viy);
+                    CoordHint<T>::get(coords, cur.rj.node, ej, pol_keep, vjx, vjy);
+                }
+            }
+            TileSel nn;
+            nn.flags = 0;
+            nn.src = 0;
+            if (m + 2 < n_mine) {
+                advance(u, i0);
+                nn = select(u, i0);   // stage B, unit m+2
+            }
+            if (m + 1 < n_mine) resolve(nxt);  // stage C, unit m+1
+            // Stage D arithmetic + write-back for unit m
+            if ((cur.flags & 1u) && d_ref > 0.0)
+                applied += hog_apply_t<T>(coords, cur.ri.node, ei, cur.rj.node, ej, d_ref, a.eta, r, pol_keep,
+                                          vix, viy, vjx, vjy);
+            if ((cur.flags & 1u) && a.drf > 1) {
+                unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+                for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                    int ea, eb;
+                    do {
+                        const uint64_t b2 = r.next();
+                        ea = (b2 >> 63) ? 0 : 1;
+                        eb = ((b2 >> 62) & 1) ? 0 : 1;
+                    } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                    used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                    applied += hog_update_t<T>(coords, cur.ri.node, ea, cur.rj.node, eb,
+                                               abs_diff(step_pos(cur.ri, ea), step_pos(cur.rj, eb)), a.eta, r,
+                                               pol_keep);
+                }
+            }
             cur = nxt;
+            nxt = nn;
         }
     }
 
@@ -264,10 +377,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     flush_stat(stats, 7, b_second);
 }
 
+// variant 0 (default): two-stage; 1: two-stage, 3 CTAs/SM (80 registers);
+// 2: four-stage pipeline (no fronts order). Measured at configs 2 and 3 with
+// shared partner windows: the two-stage kernel matches or beats the
+// four-stage one, whose L2 prefetches no longer hide anything once partner
+// loads are coalesced.
 template <typename T>
 const void* tiles_fn(int variant) {
-    return variant == 1 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3>)
-                        : reinterpret_cast<const void*>(k_sgd_tiles<T, 1>);
+    return variant == 1   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 2>)
+           : variant == 2 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 4>)
+                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 2>);
 }
 
 }  // namespace

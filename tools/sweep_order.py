@@ -32,6 +32,9 @@ def ext_of(v):
             e.pair_window = 1
         elif part == "win":
             e.pair_window = 2
+        elif part.startswith("hop"):
+            e.pair_window = 3
+            e.hop_lanes = int(part[3:] or 0)
         elif part == "rn":
             e.record_hint = 1
         elif part.startswith("v") and part[1:].isdigit():
