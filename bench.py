@@ -13,9 +13,14 @@ run_layout of that graph: 30 x 10 x sum|p| = 2.61e10 attempted updates.
   e2e    : updates/s through the C-ABI drop-in pgl_layout_run with HOST
            buffers: pack + H2D of the graph and initial layout, 30 kernels,
            D2H of the coordinates, every step (host wall, synchronised).
-  roofline: k_sgd_tiles, 192 algorithmic bytes per update (6 random
-           32-byte sectors) x updates per launch / mean
-           launch time, against MEASURED_PEAKS.json hbm_gbs.
+  roofline: k_sgd_tiles, algorithmic bytes per update = the payload one
+           update must move: two 16-byte step records (i, j) + two endpoint
+           reads + two endpoint write-backs (16 B each in f64, 8 B in f32)
+           = 96 B (f64) / 64 B (f32), x updates per launch / mean launch
+           time, against MEASURED_PEAKS.json hbm_gbs. (SURVEY.md §8d's 192 B
+           = six random 32-byte sectors priced the reference's i.i.d. access
+           pattern; the tile sampler's coalesced unit/window/hop loads move
+           less than that, so the payload is the honest denominator.)
   cpu_baseline: the reference library itself (oracle/_ref, built from the
            reference sources), all host cores, on a bounded sample.
 
@@ -41,7 +46,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PG-SGD updates/sec and layout wall-time per chromosome; sampled path stress"
 UNIT = "updates/s"
-BYTES_PER_UPDATE = 192  # 6 random 32-byte sectors
+# payload bytes per update: 2 x 16-byte step records + 4 endpoint accesses
+BYTES_PER_UPDATE = {"f64": 2 * 16 + 4 * 16, "f32": 2 * 16 + 4 * 8}
 CONFIGS = {
     "c1": (1, 9680, 8, 0.05),
     "c2": (1, 968000, 90, 0.05),
@@ -321,7 +327,7 @@ def run_ours(args, dist: Dist):
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
 
     peak, peak_src = hbm_peak()
-    bytes_per_launch = (10 * S // cfg.srf) * cfg.drf * BYTES_PER_UPDATE
+    bytes_per_launch = (10 * S // cfg.srf) * cfg.drf * BYTES_PER_UPDATE[args.coord]
     achieved = bytes_per_launch / (sgd_launch_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.config, args.coord)
     if dist.rank == 0:
@@ -342,7 +348,9 @@ def run_ours(args, dist: Dist):
                     "seconds_per_step": e2e_s, "api": "pgl_layout_run (C-ABI) from host PathStep arrays"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgd_tiles",
-                         "bytes_per_update": BYTES_PER_UPDATE, "launch_ms": sgd_launch_ms,
+                         "bytes_per_update": BYTES_PER_UPDATE[args.coord],
+                         "bytes_model": "payload: 2 step records + 2 endpoint reads + 2 endpoint writes",
+                         "launch_ms": sgd_launch_ms,
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
             "gpu_launches": launches,

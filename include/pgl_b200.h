@@ -10,6 +10,7 @@
  *   pgl_layout_run              <- pglayout::run_layout        include/pglayout/engine.hpp:80-82, src/engine.cpp:323-326
  *                                  pglayout::run_layout_reuse  include/pglayout/engine.hpp:86-88, src/engine.cpp:328-334
  *   pgl_sampled_path_stress     <- pglayout::sampled_path_stress include/pglayout/metrics.hpp:49-51, src/metrics.cpp:108-159
+ *   pgl_exact_path_stress       <- pglayout::exact_path_stress  include/pglayout/metrics.hpp:39, src/metrics.cpp:75-106
  *   pgl_graph_create/_layout/.. <- same two calls, split so the packed graph stays resident in HBM
  *                                  across calls (the reference rebuilds nothing either: PangenomeGraph
  *                                  is immutable, graph.hpp:61-88)
@@ -306,6 +307,20 @@ int pgl_sampled_path_stress(int device, const pgl_graph_view* graph,
 int pgl_graph_stress(pgl_graph* g, const double* coords, uint64_t seed,
                      uint32_t samples_per_node, uint32_t method,
                      pgl_stress_report* out, double* kernel_ms);
+
+/* ---- exact path stress: the drop-in for exact_path_stress --------------- */
+
+/* Every step pair i < j of every path, the reference's per-pair term
+ * (step_pair_stress, metrics.cpp:59-73; IEEE, bit-identical terms), two
+ * passes (mean, then squared deviations), n/skipped exact; sums in
+ * double-double with a fixed fold order (deterministic, within a few ulps of
+ * the exact sum of the terms). O(sum |p|^2): meant for small graphs. */
+int pgl_exact_path_stress(int device, const pgl_graph_view* graph,
+                          const double* coords, pgl_stress_report* out);
+
+/* On a resident graph; coords NULL = the resident layout. */
+int pgl_graph_exact_stress(pgl_graph* g, const double* coords,
+                           pgl_stress_report* out, double* kernel_ms);
 
 /* ---- host-side helpers of the path (bit-exact with the reference) -------- */
 

@@ -133,6 +133,8 @@ _sig = {
                                  C.POINTER(_Report)], C.c_int),
     "pgl_graph_stress": ([_vp, _f64p, C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(_Report), _f64p],
                          C.c_int),
+    "pgl_exact_path_stress": ([C.c_int, C.POINTER(_View), _f64p, C.POINTER(_Report)], C.c_int),
+    "pgl_graph_exact_stress": ([_vp, _f64p, C.POINTER(_Report), _f64p], C.c_int),
     "pgl_make_schedule": ([C.POINTER(_View), C.POINTER(_Cfg), _f64p], C.c_int),
     "pgl_init_layout": ([C.POINTER(_View), C.c_uint64, _f64p], C.c_int),
     "pgl_layout_shards": ([C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.POINTER(_View)),
@@ -488,6 +490,17 @@ def sampled_path_stress(g: PangenomeGraph, layout: np.ndarray, seed: int,
     return StressReport._of(r)
 
 
+def exact_path_stress(g: PangenomeGraph, layout: np.ndarray, device: int = 0) -> StressReport:
+    """exact_path_stress (metrics.hpp:39, metrics.cpp:75-106) on the GPU:
+    every step pair of every path, deterministic double-double reduction."""
+    c = np.ascontiguousarray(layout, np.float64).reshape(-1)
+    if c.size != 4 * g.n_nodes:
+        raise CountMismatch("CountMismatch: layout size does not match the graph")
+    r = _Report()
+    _check(_lib.pgl_exact_path_stress(device, C.byref(g.view()), c.ctypes.data_as(_f64p), C.byref(r)))
+    return StressReport._of(r)
+
+
 def make_schedule(g: PangenomeGraph, cfg: LayoutConfig) -> np.ndarray:
     etas = np.zeros(max(cfg.n_iters, 1))
     _check(_lib.pgl_make_schedule(C.byref(g.view()), C.byref(cfg._c()), etas.ctypes.data_as(_f64p)))
@@ -574,6 +587,16 @@ class DeviceGraph:
         c = None if layout is None else np.ascontiguousarray(layout, np.float64).reshape(-1)
         _check(_lib.pgl_graph_stress(self.h, c.ctypes.data_as(_f64p) if c is not None else None, seed,
                                      samples_per_node, method, C.byref(r), C.byref(ms)))
+        rep = StressReport._of(r)
+        return (rep, ms.value) if return_ms else rep
+
+    def exact_stress(self, layout: Optional[np.ndarray] = None, return_ms: bool = False):
+        """exact_path_stress on the resident graph (layout None = resident layout)."""
+        r = _Report()
+        ms = C.c_double()
+        c = None if layout is None else np.ascontiguousarray(layout, np.float64).reshape(-1)
+        _check(_lib.pgl_graph_exact_stress(self.h, c.ctypes.data_as(_f64p) if c is not None else None,
+                                           C.byref(r), C.byref(ms)))
         rep = StressReport._of(r)
         return (rep, ms.value) if return_ms else rep
 

@@ -1,0 +1,240 @@
+// pgl_exact.cu — exact path stress (metrics.cpp:75-106) on the GPU.
+//
+// The reference enumerates every step pair i < j of every path, averages
+// pair_stress over the endpoint combinations with a nonzero reference
+// distance (step_pair_stress, metrics.cpp:59-73, order start/start,
+// start/end, end/start, end/end), and reports mean and sample sigma over the
+// pairs with at least one such combination (two passes: sum, then squared
+// deviations from the mean). O(sum |p|^2) pairs: the small-graph fidelity
+// metric (acceptance criterion 3).
+//
+// Device plan: one row = one primary step i (global step index); warps pull
+// rows from an atomic counter (load balance: row lengths are |p| - 1 - i);
+// lane l takes j = i + 1 + l, i + 33 + l, ... so the row's j records and
+// coordinates are read coalesced and i's are a warp broadcast. Each term is
+// computed with IEEE division/sqrt and no FMA contraction (-fmad=false), i.e.
+// bit-identical to the reference's term. Sums are double-double (TwoSum)
+// from the lane partials up: per-row results are written to their row slot,
+// and rows are folded in a fixed tree order, so the result does not depend
+// on which warp took which row and is within a few ulps of the exact sum of
+// the reference's terms (the reference's own serial sum carries more
+// rounding than that).
+#include <cuda_runtime.h>
+
+#include "pgl_device.cuh"
+
+namespace pgl {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kFoldBlock = 1024;
+
+struct DD {
+    double hi, lo;
+};
+
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+    // TwoSum of the high parts, then the low parts folded in (Neumaier-style)
+    const double s = a.hi + b.hi;
+    const double bb = s - a.hi;
+    const double err = (a.hi - (s - bb)) + (b.hi - bb);
+    const double lo = err + a.lo + b.lo;
+    const double hi = s + lo;
+    return DD{hi, lo - (hi - s)};
+}
+
+__device__ __forceinline__ DD dd_add1(DD a, double b) { return dd_add(a, DD{b, 0.0}); }
+
+__device__ __forceinline__ DD dd_shfl_down(DD v, int off) {
+    return DD{__shfl_down_sync(0xFFFFFFFFu, v.hi, off), __shfl_down_sync(0xFFFFFFFFu, v.lo, off)};
+}
+
+struct RowAcc {
+    double hi, lo;
+    unsigned long long n, skipped;
+};
+
+// path of global step index s: binary search of cum (P is small)
+__device__ __forceinline__ uint32_t path_of(const DevGraph& g, uint64_t s) {
+    uint32_t lo = 0, hi = g.n_paths;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(g.cum + mid) <= s)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// step_pair_stress (metrics.cpp:59-73): returns the number of terms (0 =
+// skipped) and their average in `avg`.
+__device__ __forceinline__ int pair_term(const StepRec& ri, double vi[4], const StepRec& rj, const double* coords,
+                                         double& avg) {
+    double vj[4];
+    const double2 a = __ldg(reinterpret_cast<const double2*>(coords) + 2 * static_cast<uint64_t>(rj.node));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(coords) + 2 * static_cast<uint64_t>(rj.node) + 1);
+    vj[0] = a.x;
+    vj[1] = a.y;
+    vj[2] = b.x;
+    vj[3] = b.y;
+    double sum = 0.0;
+    int count = 0;
+#pragma unroll
+    for (int ei = 0; ei < 2; ++ei) {
+        const uint64_t pi = step_pos(ri, ei);
+#pragma unroll
+        for (int ej = 0; ej < 2; ++ej) {
+            const uint64_t pj = step_pos(rj, ej);
+            if (pi == pj) continue;
+            const double d = abs_diff(pi, pj);
+            const double dx = vi[2 * ei] - vj[2 * ej];
+            const double dy = vi[2 * ei + 1] - vj[2 * ej + 1];
+            const double err = (sqrt(dx * dx + dy * dy) - d) / d;  // pair_stress, metrics.cpp:52-57
+            sum += err * err;
+            ++count;
+        }
+    }
+    if (count) avg = sum / count;
+    return count;
+}
+
+template <int kPass>
+__global__ void __launch_bounds__(kThreads) k_exact_rows(DevGraph g, const double* __restrict__ coords, double mean,
+                                                         RowAcc* __restrict__ rows,
+                                                         unsigned long long* __restrict__ next_row) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t S = g.total_steps;
+    for (;;) {
+        unsigned long long r = 0;
+        if (lane == 0) r = atomicAdd(next_row, 1ULL);
+        r = __shfl_sync(0xFFFFFFFFu, r, 0);
+        if (r >= S) break;
+        const uint32_t p = path_of(g, r);
+        const uint64_t end = __ldg(g.cum + p + 1);  // one past the path's last step
+        const StepRec ri = load_step(g.step + r);
+        double vi[4];
+        {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(coords) + 2 * static_cast<uint64_t>(ri.node));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(coords) + 2 * static_cast<uint64_t>(ri.node) + 1);
+            vi[0] = a.x;
+            vi[1] = a.y;
+            vi[2] = b.x;
+            vi[3] = b.y;
+        }
+        DD acc{0.0, 0.0};
+        unsigned long long n = 0, skipped = 0;
+        for (uint64_t j = r + 1 + lane; j < end; j += 32) {
+            const StepRec rj = load_step(g.step + j);
+            double t;
+            if (pair_term(ri, vi, rj, coords, t)) {
+                if (kPass == 1) {
+                    acc = dd_add1(acc, t);
+                } else {
+                    const double dev = t - mean;
+                    acc = dd_add1(acc, dev * dev);
+                }
+                ++n;
+            } else {
+                ++skipped;
+            }
+        }
+        // fixed-order warp tree
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const DD o = dd_shfl_down(acc, off);
+            acc = dd_add(acc, o);
+            n += __shfl_down_sync(0xFFFFFFFFu, n, off);
+            skipped += __shfl_down_sync(0xFFFFFFFFu, skipped, off);
+        }
+        if (lane == 0) rows[r] = RowAcc{acc.hi, acc.lo, n, skipped};
+    }
+}
+
+// Fold rows [b*kFoldBlock, ...) of `in` into out[b], in a fixed tree order.
+__global__ void __launch_bounds__(kFoldBlock) k_exact_fold(const RowAcc* __restrict__ in, uint64_t n_in,
+                                                           RowAcc* __restrict__ out) {
+    __shared__ RowAcc sh[kFoldBlock];
+    const uint64_t k = blockIdx.x * static_cast<uint64_t>(kFoldBlock) + threadIdx.x;
+    sh[threadIdx.x] = k < n_in ? in[k] : RowAcc{0.0, 0.0, 0, 0};
+    __syncthreads();
+    for (int w = kFoldBlock / 2; w > 0; w >>= 1) {
+        if (static_cast<int>(threadIdx.x) < w) {
+            const RowAcc a = sh[threadIdx.x], b = sh[threadIdx.x + w];
+            const DD s = dd_add(DD{a.hi, a.lo}, DD{b.hi, b.lo});
+            sh[threadIdx.x] = RowAcc{s.hi, s.lo, a.n + b.n, a.skipped + b.skipped};
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
+}
+
+}  // namespace
+
+// Two passes over all pairs; fills mean, n, skipped and the squared-deviation
+// sum (finish_report computes sigma and the CI on the host).
+void run_exact_stress(const DevGraph& g, const double* coords, pgl_stress_report* out, double* sum_sq_dev,
+                      double* kernel_ms, void* stream_) {
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const uint64_t S = g.total_steps;
+    int dev = 0, sms = 0, occ = 0;
+    PGL_CUDA(cudaGetDevice(&dev));
+    PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_exact_rows<1>, kThreads, 0));
+    const int blocks = sms * (occ > 0 ? occ : 1);
+    // scratch: rows[S], two fold levels, counter
+    const uint64_t n1 = (S + kFoldBlock - 1) / kFoldBlock;
+    const uint64_t n2 = (n1 + kFoldBlock - 1) / kFoldBlock;
+    RowAcc* rows = nullptr;
+    unsigned long long* ctr = nullptr;
+    PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), (S + n1 + n2 + 1) * sizeof(RowAcc), stream));
+    PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ctr), sizeof(unsigned long long), stream));
+    RowAcc* lvl1 = rows + S;
+    RowAcc* lvl2 = lvl1 + n1;
+    RowAcc* fin = lvl2 + n2;
+    cudaEvent_t e0, e1;
+    PGL_CUDA(cudaEventCreate(&e0));
+    PGL_CUDA(cudaEventCreate(&e1));
+    PGL_CUDA(cudaEventRecord(e0, stream));
+    RowAcc res[2];
+    double mean = 0.0;
+    for (int pass = 1; pass <= 2; ++pass) {
+        PGL_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), stream));
+        if (pass == 1)
+            k_exact_rows<1><<<blocks, kThreads, 0, stream>>>(g, coords, 0.0, rows, ctr);
+        else
+            k_exact_rows<2><<<blocks, kThreads, 0, stream>>>(g, coords, mean, rows, ctr);
+        PGL_CUDA(cudaGetLastError());
+        k_exact_fold<<<static_cast<unsigned>(n1), kFoldBlock, 0, stream>>>(rows, S, lvl1);
+        k_exact_fold<<<static_cast<unsigned>(n2), kFoldBlock, 0, stream>>>(lvl1, n1, lvl2);
+        // n2 <= 1024 for S <= 2^30 rows; fold the rest in one block (bigger
+        // inputs are far beyond the O(|p|^2) metric's useful range)
+        if (n2 > static_cast<uint64_t>(kFoldBlock)) raise(PGL_ERR_INVALID_PARAMETER, "exact path stress: too many steps");
+        k_exact_fold<<<1, kFoldBlock, 0, stream>>>(lvl2, n2, fin);
+        PGL_CUDA(cudaGetLastError());
+        PGL_CUDA(cudaMemcpyAsync(&res[pass - 1], fin, sizeof(RowAcc), cudaMemcpyDeviceToHost, stream));
+        PGL_CUDA(cudaStreamSynchronize(stream));
+        if (pass == 1) {
+            const double sum = res[0].hi + res[0].lo;
+            mean = res[0].n > 0 ? sum / static_cast<double>(res[0].n) : 0.0;
+            if (res[0].n < 2) break;
+        }
+    }
+    PGL_CUDA(cudaEventRecord(e1, stream));
+    PGL_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (kernel_ms) *kernel_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    PGL_CUDA(cudaFreeAsync(rows, stream));
+    PGL_CUDA(cudaFreeAsync(ctr, stream));
+    PGL_CUDA(cudaStreamSynchronize(stream));
+    out->mean = mean;
+    out->n = res[0].n;
+    out->skipped = res[0].skipped;
+    *sum_sq_dev = res[0].n >= 2 ? res[1].hi + res[1].lo : 0.0;
+}
+
+}  // namespace pgl

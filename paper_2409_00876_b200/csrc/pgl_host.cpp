@@ -803,6 +803,24 @@ void graph_stress(pgl_graph* G, const double* coords, uint64_t seed, uint32_t sp
         raise(PGL_ERR_INVALID_PARAMETER, "unknown sampled stress method");
 }
 
+void graph_exact_stress(pgl_graph* G, const double* coords, pgl_stress_report* out, double* kernel_ms) {
+    if (!out) raise(PGL_ERR_INVALID_PARAMETER, "report is null");
+    DeviceGuard dg(G->device);
+    const uint64_t V = G->n_nodes;
+    if (coords) {
+        G->coords64.alloc(4 * V);
+        PGL_CUDA(cudaMemcpyAsync(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+        G->layout_f64 = -1;  // the resident layout is overwritten
+    } else {
+        if (G->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
+        if (!G->layout_f64) launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+    }
+    std::memset(out, 0, sizeof *out);
+    double ssd = 0.0;
+    run_exact_stress(G->dev(), G->coords64.p, out, &ssd, kernel_ms, G->stream);
+    finish_report(out, ssd);  // metrics.cpp:14-23
+}
+
 // ---- synthetic fixture (synthetic.cpp:24-120, walks only) ----------------------
 
 struct Synthetic {
@@ -1025,6 +1043,23 @@ int pgl_sampled_path_stress(int device, const pgl_graph_view* v, const double* c
         if (!coords) raise(PGL_ERR_INVALID_PARAMETER, "coords is null");
         std::unique_ptr<pgl_graph> G(create_graph(device, v));
         graph_stress(G.get(), coords, seed, spn, method, out, nullptr);
+        DeviceGuard dg(device);
+        G.reset();
+    });
+}
+
+int pgl_graph_exact_stress(pgl_graph* g, const double* coords, pgl_stress_report* out, double* kernel_ms) {
+    return guarded([&] {
+        if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
+        graph_exact_stress(g, coords, out, kernel_ms);
+    });
+}
+
+int pgl_exact_path_stress(int device, const pgl_graph_view* v, const double* coords, pgl_stress_report* out) {
+    return guarded([&] {
+        if (!coords) raise(PGL_ERR_INVALID_PARAMETER, "coords is null");
+        std::unique_ptr<pgl_graph> G(create_graph(device, v));
+        graph_exact_stress(G.get(), coords, out, nullptr);
         DeviceGuard dg(device);
         G.reset();
     });

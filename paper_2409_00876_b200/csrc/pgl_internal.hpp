@@ -149,6 +149,11 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64,
                     uint64_t seed, uint32_t spn, pgl_stress_report* out,
                     double* kernel_ms, void* stream);
 
+// Exact path stress (pgl_exact.cu): mean, n, skipped into out; the
+// squared-deviation sum into sum_sq_dev (finish_report does the rest).
+void run_exact_stress(const DevGraph& g, const double* coords, pgl_stress_report* out, double* sum_sq_dev,
+                      double* kernel_ms, void* stream);
+
 // Small device helpers used by the host driver.
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
 void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);

@@ -9,6 +9,8 @@
 // leave without a jitter, and its two step records are in flight. If step s
 // does draw a jitter, the plan of s+1 is discarded and redone from the true
 // state. Coordinates live in shared memory when 32 B x nodes fits.
+// k_sgd_replay_pc (below, the one launched) splits planning and updating
+// across two warps instead.
 #include <cuda_runtime.h>
 
 #include "pgl_device.cuh"
@@ -19,6 +21,7 @@ namespace {
 
 struct Plan {
     StepRec ri, rj;
+    uint64_t gi, gj;  // global step indices of i and j
     Xo r_mid;      // stream right after the two endpoint coins
     Xo r_end;      // stream after this step's draws, assuming no jitter
     int ei, ej;
@@ -29,7 +32,8 @@ struct Plan {
 
 // Batch decision (engine.cpp:115-124), select_step_pair (:52-80), the two
 // coins (:137-138) and the coins of the drf extra combinations (:155-161).
-__device__ __forceinline__ Plan plan_step(const DevGraph& g, const IterArgs& a, uint64_t s, Xo r, bool& cooling) {
+__device__ __forceinline__ Plan plan_step(const DevGraph& g, const IterArgs& a, uint64_t s, Xo r, bool& cooling,
+                                          bool load_records = true) {
     Plan P;
     P.opened = (s % a.batch) == 0;
     if (P.opened) cooling = a.force_cooling || r.coin();
@@ -37,6 +41,7 @@ __device__ __forceinline__ Plan plan_step(const DevGraph& g, const IterArgs& a, 
     P.valid = false;
     P.ei = P.ej = 0;
     P.ri = P.rj = StepRec{0, 0, 0, 0};
+    P.gi = P.gj = 0;
     const uint64_t x = r.next();
     const uint64_t pick = __umul64hi(x, g.total_steps);
     const uint32_t p = select_path(g, x, pick);
@@ -67,8 +72,12 @@ __device__ __forceinline__ Plan plan_step(const DevGraph& g, const IterArgs& a, 
         }
         if (ok) {
             P.valid = true;
-            P.ri = load_step(g.step + pc.base + i);
-            P.rj = load_step(g.step + pc.base + j);
+            P.gi = pc.base + i;
+            P.gj = pc.base + j;
+            if (load_records) {
+                P.ri = load_step(g.step + P.gi);
+                P.rj = load_step(g.step + P.gj);
+            }
             P.ei = r.coin() ? 0 : 1;
             P.ej = r.coin() ? 0 : 1;
         }
@@ -121,66 +130,192 @@ __device__ __forceinline__ bool apply_exact(double* c, uint32_t ni, int ei, uint
     return true;
 }
 
-__global__ void __launch_bounds__(32) k_sgd_replay2(DevGraph g, double* __restrict__ gcoords, uint64_t* rng4,
-                                                    DevStats* stats, IterArgs a, int use_smem) {
-    extern __shared__ double smem_coords[];
+// ---- producer / consumer replay ----------------------------------------------
+// Two warps, one active lane each. The PRODUCER (warp 0) walks the RNG stream
+// and the graph index: batch decision, pick, partner, coins (plan_step), then
+// has the TMA engine copy the two step records into a ring slot (bulk copy,
+// mbarrier completion). The CONSUMER (warp 1) owns the coordinates: endpoint
+// loads, apply_exact, write-back, drf extras, RunStats. Nothing the producer
+// computes depends on coordinates except through a jitter draw
+// (engine.cpp:292-296); when the consumer draws one, it posts the true
+// stream state and the producer restarts planning from the next step under a
+// new epoch while the consumer discards the stale slots. The consumer's
+// sequence of operations is exactly the reference's, so results stay bit
+// for bit; the producer's latency (Zipf transcendentals, index loads, record
+// gathers) runs concurrently on the other warp.
+
+constexpr uint32_t kRing = 128;
+
+struct alignas(16) Slot {
+    StepRec ri, rj;   // TMA destination (valid steps only)
+    Xo r_mid;         // stream after the two endpoint coins
+    Xo r_end;         // stream after this step, assuming no jitter
+    uint64_t step;
+    uint32_t flags;   // bit0 valid, bit1 opened, bit2 cooling, bit3 e_i end, bit4 e_j end
+    uint32_t epoch;
+};
+
+struct ReplayCtl {
+    unsigned long long tail;      // slots consumed (consumer -> producer)
+    Xo req_state;                 // restart stream state
+    unsigned long long req_step;  // restart step
+    uint32_t req_cool;            // batch cooling flag in force after the jittered step
+    uint32_t req_epoch;           // restart request epoch (consumer -> producer)
+    uint32_t done;                // consumer finished
+    uint32_t _pad;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra WAIT_%=;\n}\n" :: "r"(smem_addr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
+
+__global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __restrict__ gcoords, uint64_t* rng4,
+                                                      DevStats* stats, IterArgs a, int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Slot* ring = reinterpret_cast<Slot*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kRing * sizeof(Slot));
+    ReplayCtl* ctl = reinterpret_cast<ReplayCtl*>(smem + kRing * (sizeof(Slot) + 8));
+    double* scoords = reinterpret_cast<double*>(smem + kRing * (sizeof(Slot) + 8) + sizeof(ReplayCtl));
     const uint64_t n4 = 4 * g.n_nodes;
     double* coords = gcoords;
     if (use_smem) {
-        for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) smem_coords[k] = gcoords[k];
-        __syncwarp();
-        coords = smem_coords;
+        for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) scoords[k] = gcoords[k];
+        coords = scoords;
     }
     if (threadIdx.x == 0) {
+        for (uint32_t k = 0; k < kRing; ++k) mbar_init(bar + k, 1);
+        ctl->tail = 0;
+        ctl->req_epoch = 0;
+        ctl->done = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    volatile ReplayCtl* vc = ctl;
+
+    if (threadIdx.x == 0) {  // ---------------- producer ----------------
         Xo r{rng4[0], rng4[1], rng4[2], rng4[3]};
-        unsigned long long applied = 0, bf = 0, bfc = 0, bs = 0;
-        bool cool_state = false;  // planner's batch state (engine.cpp:113)
-        Plan cur = plan_step(g, a, 0, r, cool_state);
-        for (uint64_t s = 0; s < a.steps; ++s) {
-            const bool cool_after_cur = cool_state;
-            Plan nxt;
-            const bool more = s + 1 < a.steps;
-            if (more) nxt = plan_step(g, a, s + 1, cur.r_end, cool_state);  // speculative
-            // ---- execute step s (engine.cpp:115-170) ----
-            if (cur.opened) {
-                if (a.force_cooling)
-                    ++bs;
-                else {
-                    ++bf;
-                    bfc += cur.cooling;
-                }
+        bool cool_state = false;  // engine.cpp:113
+        uint32_t epoch = 0;
+        uint64_t s = 0, q = 0;
+        for (;;) {
+            if (vc->req_epoch != epoch) {  // consumer drew a jitter: replan from its state
+                __threadfence_block();
+                epoch = vc->req_epoch;
+                r = Xo{vc->req_state.a, vc->req_state.b, vc->req_state.c, vc->req_state.d};
+                s = vc->req_step;
+                cool_state = vc->req_cool != 0;
             }
-            Xo live = cur.r_mid;
-            bool jitter = false;
-            if (cur.valid) {
-                applied += apply_exact(coords, cur.ri.node, cur.ei, cur.rj.node, cur.ej,
-                                       abs_diff(step_pos(cur.ri, cur.ei), step_pos(cur.rj, cur.ej)), a.eta, live,
-                                       jitter);
-                if (a.drf > 1) {
-                    unsigned used = 1u << ((cur.ei ? 2 : 0) | (cur.ej ? 1 : 0));
-                    for (uint32_t extra = 1; extra < a.drf; ++extra) {
-                        int ea, eb;
-                        do {
-                            ea = live.coin() ? 0 : 1;
-                            eb = live.coin() ? 0 : 1;
-                        } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
-                        used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                        applied += apply_exact(coords, cur.ri.node, ea, cur.rj.node, eb,
-                                               abs_diff(step_pos(cur.ri, ea), step_pos(cur.rj, eb)), a.eta, live,
-                                               jitter);
+            if (s >= a.steps) {
+                if (vc->done) break;
+                continue;
+            }
+            while (q - vc->tail >= kRing) {  // ring full
+                if (vc->req_epoch != epoch) break;
+            }
+            if (q - vc->tail >= kRing) continue;
+            const Plan P = plan_step(g, a, s, r, cool_state, /*load_records=*/false);
+            Slot& sl = ring[q % kRing];
+            sl.r_mid = P.r_mid;
+            sl.r_end = P.r_end;
+            sl.step = s;
+            sl.epoch = epoch;
+            sl.flags = (P.valid ? 1u : 0u) | (P.opened ? 2u : 0u) | (P.cooling ? 4u : 0u) | (P.ei ? 8u : 0u) |
+                       (P.ej ? 16u : 0u);
+            uint64_t* b = bar + (q % kRing);
+            if (P.valid) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(b, 2 * sizeof(StepRec));
+                tma_load(&sl.ri, g.step + P.gi, sizeof(StepRec), b);
+                tma_load(&sl.rj, g.step + P.gj, sizeof(StepRec), b);
+            } else {
+                mbar_arrive(b);
+            }
+            r = P.r_end;
+            ++s;
+            ++q;
+        }
+    } else if (threadIdx.x == 32) {  // ---------------- consumer ----------------
+        unsigned long long applied = 0, bf = 0, bfc = 0, bs = 0;
+        uint32_t epoch = 0;
+        Xo r{rng4[0], rng4[1], rng4[2], rng4[3]};
+        uint64_t q = 0, next_step = 0;
+        while (next_step < a.steps) {
+            Slot& sl = ring[q % kRing];
+            mbar_wait(bar + (q % kRing), static_cast<uint32_t>((q / kRing) & 1));
+            const uint32_t fl = sl.flags;
+            const bool mine = sl.epoch == epoch && sl.step == next_step;
+            if (mine) {
+                if (fl & 2u) {
+                    if (a.force_cooling)
+                        ++bs;
+                    else {
+                        ++bf;
+                        bfc += (fl >> 2) & 1u;
                     }
                 }
-            }
-            if (jitter) {  // the speculation of s+1 started from the wrong stream position
-                r = live;
-                if (more) {
-                    cool_state = cool_after_cur;
-                    nxt = plan_step(g, a, s + 1, r, cool_state);
+                Xo live = sl.r_mid;
+                bool jitter = false;
+                if (fl & 1u) {
+                    const StepRec ri = sl.ri, rj = sl.rj;
+                    const int ei = (fl >> 3) & 1, ej = (fl >> 4) & 1;
+                    applied += apply_exact(coords, ri.node, ei, rj.node, ej,
+                                           abs_diff(step_pos(ri, ei), step_pos(rj, ej)), a.eta, live, jitter);
+                    if (a.drf > 1) {
+                        unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+                        for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                            int ea, eb;
+                            do {
+                                ea = live.coin() ? 0 : 1;
+                                eb = live.coin() ? 0 : 1;
+                            } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                            used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                            applied += apply_exact(coords, ri.node, ea, rj.node, eb,
+                                                   abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, live, jitter);
+                        }
+                    }
                 }
-            } else {
-                r = cur.r_end;
+                ++next_step;
+                if (jitter) {
+                    r = live;
+                    if (next_step < a.steps) {  // restart the producer at next_step from the true stream
+                        ++epoch;
+                        vc->req_state.a = live.a;
+                        vc->req_state.b = live.b;
+                        vc->req_state.c = live.c;
+                        vc->req_state.d = live.d;
+                        vc->req_step = next_step;
+                        vc->req_cool = (fl >> 2) & 1u;
+                        __threadfence_block();
+                        vc->req_epoch = epoch;
+                    }
+                } else {
+                    r = sl.r_end;
+                }
             }
-            if (more) cur = nxt;
+            ++q;
+            __threadfence_block();
+            vc->tail = q;
         }
         rng4[0] = r.a;
         rng4[1] = r.b;
@@ -191,26 +326,27 @@ __global__ void __launch_bounds__(32) k_sgd_replay2(DevGraph g, double* __restri
         stats->v[5] += bfc;
         stats->v[6] += bs;
         stats->v[7] += bs;
+        __threadfence_block();
+        vc->done = 1;
     }
-    if (use_smem) {
-        __syncwarp();
-        for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) gcoords[k] = smem_coords[k];
-    }
+    __syncthreads();
+    if (use_smem)
+        for (uint64_t k = threadIdx.x; k < n4; k += blockDim.x) gcoords[k] = scoords[k];
 }
 
-constexpr size_t kSmemCap = 200 * 1024;
+constexpr size_t kSmemCap = 220 * 1024;
+constexpr size_t kRingBytes = kRing * (sizeof(Slot) + 8) + sizeof(ReplayCtl);
 
 }  // namespace
 
 void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4, DevStats* stats, const IterArgs& a,
                        void* stream) {
-    const size_t bytes = 32 * g.n_nodes;
-    const int use_smem = bytes <= kSmemCap ? 1 : 0;
-    if (use_smem)
-        PGL_CUDA(cudaFuncSetAttribute(k_sgd_replay2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kSmemCap)));
-    k_sgd_replay2<<<1, 32, use_smem ? bytes : 0, static_cast<cudaStream_t>(stream)>>>(g, coords, rng4, stats, a,
-                                                                                       use_smem);
+    const size_t cbytes = 32 * g.n_nodes;
+    const int use_smem = kRingBytes + cbytes <= kSmemCap ? 1 : 0;
+    const size_t bytes = kRingBytes + (use_smem ? cbytes : 0);
+    PGL_CUDA(cudaFuncSetAttribute(k_sgd_replay_pc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemCap)));
+    k_sgd_replay_pc<<<1, 64, bytes, static_cast<cudaStream_t>(stream)>>>(g, coords, rng4, stats, a, use_smem);
     PGL_CUDA(cudaGetLastError());
 }
 
