@@ -14,6 +14,8 @@
  *   pgl_graph_create/_layout/.. <- same two calls, split so the packed graph stays resident in HBM
  *                                  across calls (the reference rebuilds nothing either: PangenomeGraph
  *                                  is immutable, graph.hpp:61-88)
+ *   pgl_gfa_parse_file/_buffer  <- pglayout::parse_gfa + build_graph include/pglayout/gfa.hpp:22, src/gfa.cpp:57-153,
+ *                                  src/graph.cpp:7-59 (multithreaded; same ids, offsets, errors)
  *   pgl_make_schedule           <- pglayout::make_schedule     include/pglayout/engine.hpp:44, src/engine.cpp:266-274
  *   pgl_init_layout             <- pglayout::init_layout       include/pglayout/layout.hpp:91, src/layout.cpp:20-34
  *   pgl_last_error/_type        <- the typed exceptions of include/pglayout/errors.hpp:10-42
@@ -321,6 +323,42 @@ int pgl_exact_path_stress(int device, const pgl_graph_view* graph,
 /* On a resident graph; coords NULL = the resident layout. */
 int pgl_graph_exact_stress(pgl_graph* g, const double* coords,
                            pgl_stress_report* out, double* kernel_ms);
+
+/* ---- GFA ingest: the drop-in for parse_gfa + build_graph ----------------- */
+
+/* Edge (graph.hpp:24-30); *_end: 0 = Endpoint::start, 1 = Endpoint::end. */
+typedef struct pgl_edge {
+    uint32_t from;
+    uint32_t to;
+    uint8_t from_end;
+    uint8_t to_end;
+    uint8_t _pad[6];
+} pgl_edge;
+
+typedef struct pgl_gfa_info {
+    uint64_t n_nodes;
+    uint64_t n_edges;
+    uint64_t total_steps;
+    uint64_t skipped_records;  /* GfaParseStats::skipped_records (gfa.hpp:10-12) */
+    uint32_t n_paths;
+    uint32_t _pad0;
+} pgl_gfa_info;
+
+/* A parsed, built graph (owns its PathStep arrays). Same node ids (order of
+ * S declaration), edges (L order), paths (P order), offsets and exception
+ * classes/messages as parse_gfa followed by build_graph; the file is mmap'd
+ * and parsed on `threads` host threads (0 = all). */
+typedef struct pgl_gfa pgl_gfa;
+int pgl_gfa_parse_file(const char* path, uint32_t threads, pgl_gfa** out);
+int pgl_gfa_parse_buffer(const char* data, uint64_t size, uint32_t threads, pgl_gfa** out);
+int pgl_gfa_info_get(const pgl_gfa* g, pgl_gfa_info* out);
+/* The borrowed view for pgl_layout_run / pgl_graph_create (valid until free). */
+int pgl_gfa_view(const pgl_gfa* g, pgl_graph_view* out);
+/* Copies the n_edges edges into out. */
+int pgl_gfa_edges(const pgl_gfa* g, pgl_edge* out);
+/* Path name (P record column 2); NULL when out of range. */
+const char* pgl_gfa_path_name(const pgl_gfa* g, uint32_t path);
+int pgl_gfa_free(pgl_gfa* g);
 
 /* ---- host-side helpers of the path (bit-exact with the reference) -------- */
 

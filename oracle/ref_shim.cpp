@@ -25,6 +25,8 @@
 #include "pglayout/rng.hpp"
 #include "pglayout/synthetic.hpp"
 
+#include <chrono>
+#include <fstream>
 #include <sstream>
 
 #include "../include/pgl_b200.h"
@@ -112,6 +114,53 @@ int pglref_generate(uint64_t seed, uint64_t backbone, uint32_t paths,
         }
         *out = g;
     });
+}
+
+// parse_gfa (gfa.cpp:57-153) of an in-memory GFA text.
+int pglref_parse_gfa(const char* data, uint64_t size, void** out, uint64_t* skipped) {
+    return guarded([&] {
+        std::stringstream ss(std::string(data, size));
+        GfaParseStats st;
+        *out = new PangenomeGraph(parse_gfa(ss, &st));
+        if (skipped) *skipped = st.skipped_records;
+    });
+}
+
+// parse_gfa from a file through std::ifstream, as the CLI does
+// (tools/pglayout_main.cpp); secs = wall time of the parse.
+int pglref_parse_gfa_file(const char* path, void** out, uint64_t* skipped, double* secs) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        std::ifstream in(path);
+        if (!in) throw InvalidParameter(std::string("cannot open ") + path);
+        GfaParseStats st;
+        *out = new PangenomeGraph(parse_gfa(in, &st));
+        if (skipped) *skipped = st.skipped_records;
+        if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// write_gfa (gfa.cpp:155-178) to a file.
+int pglref_write_gfa(void* gp, const char* path) {
+    return guarded([&] {
+        std::ofstream out(path);
+        write_gfa(*static_cast<PangenomeGraph*>(gp), out);
+        if (!out) throw InvalidParameter(std::string("cannot write ") + path);
+    });
+}
+
+void pglref_edges(void* gp, uint32_t* from, uint8_t* from_end, uint32_t* to, uint8_t* to_end) {
+    const auto& g = *static_cast<PangenomeGraph*>(gp);
+    for (std::size_t k = 0; k < g.edges.size(); ++k) {
+        from[k] = g.edges[k].from;
+        to[k] = g.edges[k].to;
+        from_end[k] = g.edges[k].from_end == Endpoint::end ? 1 : 0;
+        to_end[k] = g.edges[k].to_end == Endpoint::end ? 1 : 0;
+    }
+}
+
+const char* pglref_path_name(void* gp, uint32_t p) {
+    return static_cast<PangenomeGraph*>(gp)->paths.at(p).name.c_str();
 }
 
 // build_graph (graph.cpp:7) from flat walks: step_rev[k] != 0 = reverse.

@@ -112,6 +112,15 @@ class _Timing(C.Structure):
                 ("_pad0", C.c_uint32), ("device_threads", C.c_uint64)]
 
 
+class _GfaInfo(C.Structure):
+    _fields_ = [("n_nodes", C.c_uint64), ("n_edges", C.c_uint64), ("total_steps", C.c_uint64),
+                ("skipped_records", C.c_uint64), ("n_paths", C.c_uint32), ("_pad0", C.c_uint32)]
+
+
+EDGE_DTYPE = np.dtype({"names": ["from", "to", "from_end", "to_end"],
+                       "formats": [np.uint32, np.uint32, np.uint8, np.uint8],
+                       "offsets": [0, 4, 8, 9], "itemsize": 16})
+
 _CB = C.CFUNCTYPE(C.c_int, C.c_uint32, _f64p, C.c_double, C.c_double, C.c_void_p)
 
 assert C.sizeof(_Cfg) == 56 and C.sizeof(_PathStep) == 24 and C.sizeof(_Ext) == 64
@@ -136,6 +145,13 @@ _sig = {
     "pgl_exact_path_stress": ([C.c_int, C.POINTER(_View), _f64p, C.POINTER(_Report)], C.c_int),
     "pgl_graph_exact_stress": ([_vp, _f64p, C.POINTER(_Report), _f64p], C.c_int),
     "pgl_make_schedule": ([C.POINTER(_View), C.POINTER(_Cfg), _f64p], C.c_int),
+    "pgl_gfa_parse_file": ([C.c_char_p, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "pgl_gfa_parse_buffer": ([C.c_char_p, C.c_uint64, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "pgl_gfa_info_get": ([_vp, C.POINTER(_GfaInfo)], C.c_int),
+    "pgl_gfa_view": ([_vp, C.POINTER(_View)], C.c_int),
+    "pgl_gfa_edges": ([_vp, _vp], C.c_int),
+    "pgl_gfa_path_name": ([_vp, C.c_uint32], C.c_char_p),
+    "pgl_gfa_free": ([_vp], C.c_int),
     "pgl_init_layout": ([C.POINTER(_View), C.c_uint64, _f64p], C.c_int),
     "pgl_layout_shards": ([C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.POINTER(_View)),
                            C.POINTER(_Cfg), C.POINTER(_Ext), C.POINTER(_f64p), C.POINTER(_Stats),
@@ -398,6 +414,48 @@ def generate_synthetic_pangenome(seed: int, backbone_nodes: int, n_paths: int,
     v = _View()
     _check(_lib.pgl_synthetic_view(h, C.byref(v)))
     return PangenomeGraph._from_view(v, owner)
+
+
+class _GfaOwner:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            _lib.pgl_gfa_free(self.h)
+            self.h = None
+
+
+def _gfa_graph(h) -> PangenomeGraph:
+    owner = _GfaOwner(h)
+    info = _GfaInfo()
+    _check(_lib.pgl_gfa_info_get(h, C.byref(info)))
+    v = _View()
+    _check(_lib.pgl_gfa_view(h, C.byref(v)))
+    g = PangenomeGraph._from_view(v, owner)
+    g.path_names = [_lib.pgl_gfa_path_name(h, p).decode() for p in range(info.n_paths)]
+    g.edges = np.zeros(info.n_edges, EDGE_DTYPE)
+    if info.n_edges:
+        _check(_lib.pgl_gfa_edges(h, g.edges.ctypes.data))
+    g.skipped_records = int(info.skipped_records)
+    return g
+
+
+def parse_gfa_file(path: str, threads: int = 0) -> PangenomeGraph:
+    """parse_gfa + build_graph (gfa.cpp:57-153, graph.cpp:7-59), mmap'd and
+    multithreaded: same node ids, edges, paths, offsets and exceptions.
+    The graph carries .edges (EDGE_DTYPE), .path_names, .skipped_records."""
+    h = C.c_void_p()
+    _check(_lib.pgl_gfa_parse_file(os.fsencode(path), threads, C.byref(h)))
+    return _gfa_graph(h)
+
+
+def parse_gfa(text, threads: int = 0) -> PangenomeGraph:
+    """parse_gfa of an in-memory GFA text (str or bytes)."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    _check(_lib.pgl_gfa_parse_buffer(b, len(b), threads, C.byref(h)))
+    return _gfa_graph(h)
 
 
 def build_graph(node_lengths, walks, names=None) -> PangenomeGraph:

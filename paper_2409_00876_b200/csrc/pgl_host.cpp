@@ -1065,6 +1065,61 @@ int pgl_exact_path_stress(int device, const pgl_graph_view* v, const double* coo
     });
 }
 
+struct pgl_gfa {
+    pgl::GfaGraph* g;
+};
+
+int pgl_gfa_parse_file(const char* path, uint32_t threads, pgl_gfa** out) {
+    return guarded([&] {
+        if (!path || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *out = nullptr;
+        GfaGraph* g = gfa_parse_file(path, threads);
+        *out = new pgl_gfa{g};
+    });
+}
+
+int pgl_gfa_parse_buffer(const char* data, uint64_t size, uint32_t threads, pgl_gfa** out) {
+    return guarded([&] {
+        if ((!data && size) || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *out = nullptr;
+        GfaGraph* g = gfa_parse_buffer(data ? data : "", size, threads);
+        *out = new pgl_gfa{g};
+    });
+}
+
+int pgl_gfa_info_get(const pgl_gfa* g, pgl_gfa_info* out) {
+    return guarded([&] {
+        if (!g || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        gfa_info(g->g, out);
+    });
+}
+
+int pgl_gfa_view(const pgl_gfa* g, pgl_graph_view* out) {
+    return guarded([&] {
+        if (!g || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        gfa_view(g->g, out);
+    });
+}
+
+int pgl_gfa_edges(const pgl_gfa* g, pgl_edge* out) {
+    return guarded([&] {
+        if (!g || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        pgl_gfa_info i;
+        gfa_info(g->g, &i);
+        std::memcpy(out, gfa_edges(g->g), i.n_edges * sizeof(pgl_edge));
+    });
+}
+
+const char* pgl_gfa_path_name(const pgl_gfa* g, uint32_t path) { return g ? gfa_path_name(g->g, path) : nullptr; }
+
+int pgl_gfa_free(pgl_gfa* g) {
+    if (g) {
+        gfa_free(g->g);
+        delete g;
+    }
+    return PGL_OK;
+}
+
 int pgl_make_schedule(const pgl_graph_view* v, const pgl_layout_config* cfg, double* etas) {
     return guarded([&] {
         if (!cfg || !etas) raise(PGL_ERR_INVALID_PARAMETER, "null argument");

@@ -154,6 +154,16 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64,
 void run_exact_stress(const DevGraph& g, const double* coords, pgl_stress_report* out, double* sum_sq_dev,
                       double* kernel_ms, void* stream);
 
+// GFA ingest (pgl_gfa.cpp).
+struct GfaGraph;
+GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads);
+GfaGraph* gfa_parse_file(const char* path, unsigned threads);
+void gfa_free(GfaGraph* g);
+void gfa_view(const GfaGraph* g, pgl_graph_view* v);
+void gfa_info(const GfaGraph* g, pgl_gfa_info* out);
+const pgl_edge* gfa_edges(const GfaGraph* g);
+const char* gfa_path_name(const GfaGraph* g, uint32_t p);
+
 // Small device helpers used by the host driver.
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
 void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);

@@ -256,6 +256,11 @@ class Reference:
         for name, args in {
             "pglref_generate": [C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.c_int,
                                 C.POINTER(C.c_void_p)],
+            "pglref_parse_gfa": [C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), u64p],
+            "pglref_parse_gfa_file": [C.c_char_p, C.POINTER(C.c_void_p), u64p, f64p],
+            "pglref_write_gfa": [C.c_void_p, C.c_char_p],
+            "pglref_edges": [C.c_void_p, u32p, u8p, u32p, u8p],
+            "pglref_path_name": [C.c_void_p, C.c_uint32],
             "pglref_build": [C.c_uint64, u64p, C.c_uint32, u64p, u32p, u8p, C.POINTER(C.c_void_p)],
             "pglref_free": [C.c_void_p], "pglref_counts": [C.c_void_p, u64p],
             "pglref_export": [C.c_void_p, u64p, u64p, u64p, u32p, u8p, u64p, u32p],
@@ -294,6 +299,36 @@ class Reference:
         h = C.c_void_p()
         self._check(self.lib.pglref_generate(seed, backbone, paths, rate, int(gfa_roundtrip), C.byref(h)))
         return self._wrap(h)
+
+    def parse_gfa(self, text):
+        """parse_gfa of an in-memory text -> (graph, skipped_records)."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        sk = np.zeros(1, np.uint64)
+        self._check(self.lib.pglref_parse_gfa(b, len(b), C.byref(h), ptr(sk, u64p)))
+        return self._wrap(h), int(sk[0])
+
+    def parse_gfa_file(self, path):
+        """parse_gfa through std::ifstream -> (graph, skipped_records, seconds)."""
+        h = C.c_void_p()
+        sk = np.zeros(1, np.uint64)
+        secs = np.zeros(1)
+        self._check(self.lib.pglref_parse_gfa_file(os.fsencode(path), C.byref(h), ptr(sk, u64p), ptr(secs, f64p)))
+        return self._wrap(h), int(sk[0]), float(secs[0])
+
+    def write_gfa(self, g, path):
+        self._check(self.lib.pglref_write_gfa(g.h, os.fsencode(path)))
+
+    def edges(self, g):
+        n = g.n_edges
+        f, t = np.zeros(max(n, 1), np.uint32), np.zeros(max(n, 1), np.uint32)
+        fe, te = np.zeros(max(n, 1), np.uint8), np.zeros(max(n, 1), np.uint8)
+        self.lib.pglref_edges(g.h, ptr(f, u32p), ptr(fe, u8p), ptr(t, u32p), ptr(te, u8p))
+        return f[:n], fe[:n], t[:n], te[:n]
+
+    def path_names(self, g):
+        self.lib.pglref_path_name.restype = C.c_char_p
+        return [self.lib.pglref_path_name(g.h, p).decode() for p in range(g.n_paths)]
 
     def build(self, node_len, walks):
         nl = np.asarray(node_len, np.uint64)
