@@ -176,7 +176,10 @@ struct GfaGraph {
 };
 
 GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
-    const unsigned T = std::max(1u, std::min(threads ? threads : std::thread::hardware_concurrency(), 256u));
+    // ~4 MiB of text per thread at least: thread start-up costs more than
+    // parsing a small file
+    const unsigned want = std::max(1u, std::min(threads ? threads : std::thread::hardware_concurrency(), 256u));
+    const unsigned T = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, size >> 22)));
     // ---- chunks at line boundaries ----
     const unsigned NC = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(4ull * T, size / 4096 + 1)));
     std::vector<Chunk> ch(NC);
