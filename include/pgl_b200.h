@@ -16,6 +16,8 @@
  *                                  is immutable, graph.hpp:61-88)
  *   pgl_gfa_parse_file/_buffer  <- pglayout::parse_gfa + build_graph include/pglayout/gfa.hpp:22, src/gfa.cpp:57-153,
  *                                  src/graph.cpp:7-59 (multithreaded; same ids, offsets, errors)
+ *   pgl_layout_write_tsv        <- pglayout::write_layout_tsv include/pglayout/layout_io.hpp:13, src/layout_io.cpp:31-46
+ *   pgl_layout_read_tsv         <- pglayout::read_layout_tsv  include/pglayout/layout_io.hpp:15, src/layout_io.cpp:48-110
  *   pgl_make_schedule           <- pglayout::make_schedule     include/pglayout/engine.hpp:44, src/engine.cpp:266-274
  *   pgl_init_layout             <- pglayout::init_layout       include/pglayout/layout.hpp:91, src/layout.cpp:20-34
  *   pgl_last_error/_type        <- the typed exceptions of include/pglayout/errors.hpp:10-42
@@ -359,6 +361,19 @@ int pgl_gfa_edges(const pgl_gfa* g, pgl_edge* out);
 /* Path name (P record column 2); NULL when out of range. */
 const char* pgl_gfa_path_name(const pgl_gfa* g, uint32_t path);
 int pgl_gfa_free(pgl_gfa* g);
+
+/* ---- layout table IO: the drop-in for write/read_layout_tsv -------------- */
+
+/* Byte-identical to write_layout_tsv ("%zu\t%.17g\t%.17g\t%.17g\t%.17g\n"
+ * rows under the reference header), formatted on `threads` host threads
+ * (0 = all). coords: [4*n_nodes] snapshot order. NonFiniteCoordinate names
+ * the lowest offending node, as the serial writer does. */
+int pgl_layout_write_tsv(const char* path, const double* coords, uint64_t n_nodes, uint32_t threads);
+/* read_layout_tsv: *coords receives a malloc'd [4 * *n_nodes] array (free
+ * with pgl_free); same exception classes/messages, first failure in line
+ * order. */
+int pgl_layout_read_tsv(const char* path, uint32_t threads, uint64_t* n_nodes, double** coords);
+void pgl_free(void* p);
 
 /* ---- host-side helpers of the path (bit-exact with the reference) -------- */
 

@@ -19,6 +19,7 @@
 
 #include "pglayout/engine.hpp"
 #include "pglayout/gfa.hpp"
+#include "pglayout/layout_io.hpp"
 #include "pglayout/graph.hpp"
 #include "pglayout/layout.hpp"
 #include "pglayout/metrics.hpp"
@@ -137,6 +138,28 @@ int pglref_parse_gfa_file(const char* path, void** out, uint64_t* skipped, doubl
         *out = new PangenomeGraph(parse_gfa(in, &st));
         if (skipped) *skipped = st.skipped_records;
         if (secs) *secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// write_layout_tsv / read_layout_tsv (layout_io.cpp:31-110) through files.
+int pglref_write_layout_tsv(const char* path, const double* coords, uint64_t n_nodes) {
+    return guarded([&] {
+        Layout l(n_nodes);
+        for (uint64_t n = 0; n < n_nodes; ++n) {
+            l.set(static_cast<NodeId>(n), Endpoint::start, {coords[4 * n], coords[4 * n + 1]});
+            l.set(static_cast<NodeId>(n), Endpoint::end, {coords[4 * n + 2], coords[4 * n + 3]});
+        }
+        std::ofstream out(path);
+        write_layout_tsv(l, out);
+    });
+}
+
+int pglref_read_layout_tsv(const char* path, uint64_t* n_nodes, double* coords, uint64_t cap) {
+    return guarded([&] {
+        std::ifstream in(path);
+        const Layout l = read_layout_tsv(in);
+        *n_nodes = l.node_count();
+        if (coords && 4 * l.node_count() <= cap) snapshot_into(l, coords);
     });
 }
 

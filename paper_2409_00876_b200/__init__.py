@@ -152,6 +152,9 @@ _sig = {
     "pgl_gfa_edges": ([_vp, _vp], C.c_int),
     "pgl_gfa_path_name": ([_vp, C.c_uint32], C.c_char_p),
     "pgl_gfa_free": ([_vp], C.c_int),
+    "pgl_layout_write_tsv": ([C.c_char_p, _f64p, C.c_uint64, C.c_uint32], C.c_int),
+    "pgl_layout_read_tsv": ([C.c_char_p, C.c_uint32, _u64p, C.POINTER(_f64p)], C.c_int),
+    "pgl_free": ([_vp], None),
     "pgl_init_layout": ([C.POINTER(_View), C.c_uint64, _f64p], C.c_int),
     "pgl_layout_shards": ([C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.POINTER(_View)),
                            C.POINTER(_Cfg), C.POINTER(_Ext), C.POINTER(_f64p), C.POINTER(_Stats),
@@ -456,6 +459,25 @@ def parse_gfa(text, threads: int = 0) -> PangenomeGraph:
     h = C.c_void_p()
     _check(_lib.pgl_gfa_parse_buffer(b, len(b), threads, C.byref(h)))
     return _gfa_graph(h)
+
+
+def write_layout_tsv(path: str, layout: np.ndarray, threads: int = 0) -> None:
+    """write_layout_tsv (layout_io.cpp:31-46), byte-identical, multithreaded."""
+    c = np.ascontiguousarray(layout, np.float64).reshape(-1)
+    if c.size % 4:
+        raise CountMismatch("CountMismatch: layout size is not a multiple of 4")
+    _check(_lib.pgl_layout_write_tsv(os.fsencode(path), c.ctypes.data_as(_f64p), c.size // 4, threads))
+
+
+def read_layout_tsv(path: str, threads: int = 0) -> np.ndarray:
+    """read_layout_tsv (layout_io.cpp:48-110) -> flat [4*n] snapshot-order array."""
+    n = C.c_uint64()
+    p = _f64p()
+    _check(_lib.pgl_layout_read_tsv(os.fsencode(path), threads, C.byref(n), C.byref(p)))
+    try:
+        return np.ctypeslib.as_array(p, (4 * n.value,)).copy() if n.value else np.zeros(0)
+    finally:
+        _lib.pgl_free(p)
 
 
 def build_graph(node_lengths, walks, names=None) -> PangenomeGraph:

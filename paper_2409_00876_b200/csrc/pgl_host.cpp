@@ -1120,6 +1120,29 @@ int pgl_gfa_free(pgl_gfa* g) {
     return PGL_OK;
 }
 
+int pgl_layout_write_tsv(const char* path, const double* coords, uint64_t n_nodes, uint32_t threads) {
+    return guarded([&] {
+        if (!path || (!coords && n_nodes)) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        layout_write_tsv(path, coords, n_nodes, threads);
+    });
+}
+
+int pgl_layout_read_tsv(const char* path, uint32_t threads, uint64_t* n_nodes, double** coords) {
+    return guarded([&] {
+        if (!path || !n_nodes || !coords) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *coords = nullptr;
+        *n_nodes = 0;
+        std::vector<double> v = layout_read_tsv(path, threads);
+        double* m = static_cast<double*>(std::malloc(std::max<size_t>(v.size(), 1) * sizeof(double)));
+        if (!m) throw std::bad_alloc();
+        std::memcpy(m, v.data(), v.size() * sizeof(double));
+        *coords = m;
+        *n_nodes = v.size() / 4;
+    });
+}
+
+void pgl_free(void* p) { std::free(p); }
+
 int pgl_make_schedule(const pgl_graph_view* v, const pgl_layout_config* cfg, double* etas) {
     return guarded([&] {
         if (!cfg || !etas) raise(PGL_ERR_INVALID_PARAMETER, "null argument");

@@ -164,6 +164,10 @@ void gfa_info(const GfaGraph* g, pgl_gfa_info* out);
 const pgl_edge* gfa_edges(const GfaGraph* g);
 const char* gfa_path_name(const GfaGraph* g, uint32_t p);
 
+// Layout table IO (pgl_tsv.cpp).
+void layout_write_tsv(const char* path, const double* coords, uint64_t n_nodes, uint32_t threads);
+std::vector<double> layout_read_tsv(const char* path, uint32_t threads);
+
 // Small device helpers used by the host driver.
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
 void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);

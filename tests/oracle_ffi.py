@@ -259,6 +259,8 @@ class Reference:
             "pglref_parse_gfa": [C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p), u64p],
             "pglref_parse_gfa_file": [C.c_char_p, C.POINTER(C.c_void_p), u64p, f64p],
             "pglref_write_gfa": [C.c_void_p, C.c_char_p],
+            "pglref_write_layout_tsv": [C.c_char_p, f64p, C.c_uint64],
+            "pglref_read_layout_tsv": [C.c_char_p, u64p, f64p, C.c_uint64],
             "pglref_edges": [C.c_void_p, u32p, u8p, u32p, u8p],
             "pglref_path_name": [C.c_void_p, C.c_uint32],
             "pglref_build": [C.c_uint64, u64p, C.c_uint32, u64p, u32p, u8p, C.POINTER(C.c_void_p)],
@@ -315,6 +317,16 @@ class Reference:
         secs = np.zeros(1)
         self._check(self.lib.pglref_parse_gfa_file(os.fsencode(path), C.byref(h), ptr(sk, u64p), ptr(secs, f64p)))
         return self._wrap(h), int(sk[0]), float(secs[0])
+
+    def write_layout_tsv(self, path, coords):
+        c = np.ascontiguousarray(coords, np.float64)
+        self._check(self.lib.pglref_write_layout_tsv(os.fsencode(path), ptr(c, f64p), c.size // 4))
+
+    def read_layout_tsv(self, path, cap=1 << 24):
+        n = np.zeros(1, np.uint64)
+        out = np.zeros(cap)
+        self._check(self.lib.pglref_read_layout_tsv(os.fsencode(path), ptr(n, u64p), ptr(out, f64p), cap))
+        return out[:4 * int(n[0])].copy()
 
     def write_gfa(self, g, path):
         self._check(self.lib.pglref_write_gfa(g.h, os.fsencode(path)))

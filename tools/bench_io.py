@@ -1,10 +1,13 @@
-"""GFA ingest throughput: the reference's parse_gfa
-(std::ifstream, serial; oracle/_ref) against pgl_gfa_parse_file (mmap, all
-host threads) on write_gfa output of a config graph, plus a full equality
-check of the two parsed graphs. Run on the GPU box host (its core count is
-the one the other CPU baselines use); writes one JSON line.
+"""Host IO around the path, reference vs ours
+on a config graph, with equality checks:
+  * GFA ingest: the reference's parse_gfa (std::ifstream, serial; oracle/_ref)
+    against pgl_gfa_parse_file (mmap, all host threads) on write_gfa output;
+  * layout TSV: write_layout_tsv / read_layout_tsv against
+    pgl_layout_write_tsv / pgl_layout_read_tsv (byte-identical files).
+Run on the GPU box host (its core count is the one the other CPU baselines
+use); prints (and appends to OUT) one JSON line per measurement.
 
-usage: python tools/bench_gfa.py CONFIG [OUT.json]   (CONFIG: c1 | c2 | c3)"""
+usage: python tools/bench_io.py CONFIG [OUT.jsonl]   (CONFIG: c1 | c2 | c3)"""
 import json
 import os
 import sys
@@ -54,12 +57,44 @@ def main():
            "ours_s": best, "ours_all_s": ours_s, "ours_threads": os.cpu_count(),
            "reference_MBps": size / ref_s / 1e6, "ours_MBps": size / best / 1e6,
            "speedup": ref_s / best, "identical": bool(same)}
-    print(json.dumps(rec))
-    if out:
-        with open(out, "a") as f:
-            f.write(json.dumps(rec) + "\n")
+    recs = [rec]
     os.remove(path)
+
+    # layout TSV of an init layout of the same graph
+    lay = P.init_layout(ours, 7)
+    a, b = os.path.join(d, "ours.tsv"), os.path.join(d, "ref.tsv")
+    t = time.perf_counter()
+    R.write_layout_tsv(b, lay)
+    ref_w = time.perf_counter() - t
+    ours_w = []
+    for _ in range(3):
+        t = time.perf_counter()
+        P.write_layout_tsv(a, lay)
+        ours_w.append(time.perf_counter() - t)
+    with open(a, "rb") as fa, open(b, "rb") as fb:
+        same_w = fa.read() == fb.read()
+    tsize = os.path.getsize(a)
+    t = time.perf_counter()
+    back_ref = R.read_layout_tsv(b, cap=lay.size)
+    ref_r = time.perf_counter() - t
+    ours_r = []
+    for _ in range(3):
+        t = time.perf_counter()
+        back = P.read_layout_tsv(a)
+        ours_r.append(time.perf_counter() - t)
+    recs.append({"what": "layout TSV write + read", "config": name, "tsv_bytes": tsize, "nodes": int(ours.n_nodes),
+                 "reference_write_s": ref_w, "ours_write_s": min(ours_w), "write_speedup": ref_w / min(ours_w),
+                 "reference_read_s": ref_r, "ours_read_s": min(ours_r), "read_speedup": ref_r / min(ours_r),
+                 "ours_threads": os.cpu_count(), "reference_threads": 1,
+                 "identical": bool(same_w and back.tobytes() == lay.tobytes() == back_ref.tobytes())})
+    os.remove(a)
+    os.remove(b)
     os.rmdir(d)
+    for r in recs:
+        print(json.dumps(r))
+        if out:
+            with open(out, "a") as f:
+                f.write(json.dumps(r) + "\n")
 
 
 if __name__ == "__main__":
