@@ -280,6 +280,55 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 cur = nxt;
             }
         }
+    } else if (kDepth == 3) {
+        // two-stage, with the endpoint loads of unit m issued before the
+        // selection work of unit m+1 so the latter hides their latency
+        if (n_mine) {
+            TileSel cur = select(u, i0);
+            for (uint64_t m = 0; m < n_mine; ++m) {
+                StepRec sh;
+                sh.node = __shfl_sync(kFull, cur.ri.node, cur.src);
+                sh.ps_lo = __shfl_sync(kFull, cur.ri.ps_lo, cur.src);
+                sh.pe_lo = __shfl_sync(kFull, cur.ri.pe_lo, cur.src);
+                sh.hi = __shfl_sync(kFull, cur.ri.hi, cur.src);
+                if (cur.flags & 8u) cur.rj = sh;
+                const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
+                double d_ref = 0.0, vix = 0, viy = 0, vjx = 0, vjy = 0;
+                if (cur.flags & 1u) {
+                    d_ref = abs_diff(step_pos(cur.ri, ei), step_pos(cur.rj, ej));
+                    if (d_ref > 0.0) {
+                        CoordHint<T>::get(coords, cur.ri.node, ei, pol_keep, vix, viy);
+                        CoordHint<T>::get(coords, cur.rj.node, ej, pol_keep, vjx, vjy);
+                    }
+                }
+                TileSel nxt;
+                nxt.flags = 0;
+                nxt.src = 0;
+                if (m + 1 < n_mine) {
+                    advance(u, i0);
+                    nxt = select(u, i0);
+                }
+                if ((cur.flags & 1u) && d_ref > 0.0)
+                    applied += hog_apply_t<T>(coords, cur.ri.node, ei, cur.rj.node, ej, d_ref, a.eta, r, pol_keep,
+                                              vix, viy, vjx, vjy);
+                if ((cur.flags & 1u) && a.drf > 1) {
+                    unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+                    for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                        int ea, eb;
+                        do {
+                            const uint64_t b2 = r.next();
+                            ea = (b2 >> 63) ? 0 : 1;
+                            eb = ((b2 >> 62) & 1) ? 0 : 1;
+                        } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                        used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                        applied += hog_update_t<T>(coords, cur.ri.node, ea, cur.rj.node, eb,
+                                                   abs_diff(step_pos(cur.ri, ea), step_pos(cur.rj, eb)), a.eta, r,
+                                                   pol_keep);
+                    }
+                }
+                cur = nxt;
+            }
+        }
     } else if (n_mine) {
         // Stage A: the unit's record bytes into L2 (wrapping at the end of a pass)
         auto prefetch_unit = [&](uint64_t uu, uint64_t ii) {
@@ -386,6 +435,8 @@ template <typename T>
 const void* tiles_fn(int variant) {
     return variant == 1   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 2>)
            : variant == 2 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 4>)
+           : variant == 3 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 3>)
+           : variant == 4 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 3>)
                           : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 2>);
 }
 
