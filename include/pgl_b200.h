@@ -157,8 +157,10 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t kernel_variant;  /* tile kernel: 0 = two-stage pipeline (2 CTAs/SM); 1 = two-stage,
-                                 3 CTAs/SM (80 regs); 2 = four-stage pipeline with L2 prefetch */
+    uint32_t kernel_variant;  /* tile kernel: 0 = auto; 1 = two-stage pipeline, 2 CTAs/SM;
+                                 2 = two-stage, 3 CTAs/SM; 3 = three-stage (early endpoint
+                                 loads), 3 CTAs/SM; 4 = four-stage with L2 prefetch.
+                                 i.i.d. kernel: 0 = 2 CTAs/SM, 1 = 3 CTAs/SM */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
     uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */
     uint32_t unit_order;      /* pgl_unit_order (tile sampling only) */

@@ -493,6 +493,23 @@ uint64_t next_prime(uint64_t n) {
     }
 }
 
+// Tile-kernel variant (pgl_tiles.cu): auto = the three-stage kernel at 3
+// CTAs/SM once the concurrency cap no longer binds (the graph fills the
+// GPU), else the two-stage kernel, whose shorter read-to-write window keeps
+// small graphs' layouts closest to the reference. The fronts order runs on
+// the two-stage kernel only.
+int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
+    int v = static_cast<int>(ext.kernel_variant & 15);
+    const int force64 = static_cast<int>(ext.kernel_variant & 16);
+    if (v == 0) {
+        int sms = 0;
+        PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        v = cap >= static_cast<uint32_t>(sms) * 3 * 8 ? 3 : 1;
+    }
+    if (ext.unit_order == PGL_ORDER_FRONTS && v > 2) v = 1;
+    return v | force64;
+}
+
 uint32_t auto_max_warps(uint64_t n_nodes) {
     // Hogwild concurrency cap: keep the number of in-flight updates well
     // below the number of endpoints so concurrent read-modify-writes on one
@@ -608,8 +625,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         shape = ext.sampling == PGL_SAMPLING_IID
                     ? sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
                     : tiles_shape(G->device, f64, cap, static_cast<int>(ext.block_threads),
-                                  ext.unit_order == PGL_ORDER_FRONTS && ext.kernel_variant == 2
-                                      ? 0 : static_cast<int>(ext.kernel_variant));
+                                  tile_variant(G->device, ext, cap), G->sum.total_steps);
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;

@@ -119,6 +119,7 @@ struct LaunchShape {
     int blocks = 0;
     int threads = 256;
     int variant = 0;
+    bool idx32 = false;  // tile kernel: 32-bit index instantiation
 };
 
 // Occupancy-derived persistent grid for the Hogwild kernel.
@@ -130,7 +131,8 @@ void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng r
                         void* stream);
 void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_f64, DevRng rng,
                       DevStats* stats, const IterArgs& a, LaunchShape shape, void* stream);
-LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant);
+LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant,
+                        uint64_t total_steps);
 void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4,
                        DevStats* stats, const IterArgs& a, void* stream);
 

@@ -28,6 +28,8 @@
 // trail instead of cold random lines.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "pgl_device.cuh"
 
 namespace pgl {
@@ -65,9 +67,13 @@ struct TileSel {
 //   C  unit m+1: in-tile partner records by shuffle; L2 prefetch of the two
 //                coordinate endpoints
 //   D  unit m:   endpoint loads (L2 hits), update, write-back
-template <typename T, int kMinBlocks, int kDepth>
+template <typename T, int kMinBlocks, int kDepth, bool k32>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                 DevStats* stats, IterArgs a) {
+    // k32: every step index, unit index and path length fits in 31 bits
+    // (S < 2^31): 32-bit index arithmetic, fewer registers and instructions
+    using UX = std::conditional_t<k32, uint32_t, uint64_t>;
+    using SX = std::conditional_t<k32, int32_t, int64_t>;
     const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint32_t warp = static_cast<uint32_t>(tid >> 5);
     const uint32_t lane = threadIdx.x & 31;
@@ -76,10 +82,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     Xo r{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = a.record_hint ? policy_evict_normal() : policy_evict_first();
-    const uint64_t S = g.total_steps;
-    const uint64_t U = a.units;
-    const uint64_t n_mine = warp < U ? (U - warp + a.n_warps - 1) / a.n_warps : 0;  // k = w + m*W < U
-    uint64_t u = warp < U ? (a.perm_a * static_cast<uint64_t>(warp) + a.perm_b) % U : 0;
+    const UX S = static_cast<UX>(g.total_steps);
+    const UX U = static_cast<UX>(a.units);
+    const UX n_mine = warp < U ? static_cast<UX>((U - warp + a.n_warps - 1) / a.n_warps) : 0;  // k = w + m*W < U
+    UX u = warp < U ? static_cast<UX>((a.perm_a * static_cast<uint64_t>(warp) + a.perm_b) % a.units) : 0;
     uint64_t k = warp;  // this warp's visit index, k = w + m*W
     // fronts order: unit of visit index k (see IterArgs)
     auto front_unit = [&](uint64_t kk) -> uint64_t {
@@ -89,21 +95,20 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const uint64_t uu = start + (a.reverse ? len - 1 - t : t) + a.perm_b;
         return uu >= U ? uu - U : uu;
     };
-    if (a.fronts && warp < U) u = front_unit(k);
+    if (a.fronts && warp < U) u = static_cast<UX>(front_unit(k));
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
     bool carry = false;
     uint32_t b0 = 0;  // this warp's step count mod batch (batch boundaries, engine.cpp:115-124)
 
     // Stage A: batch decision, i's record (coalesced), partner selection.
-    auto select = [&](uint64_t unit, uint64_t unit_i0) -> TileSel {
+    auto select = [&](UX unit, UX unit_i0) -> TileSel {
         TileSel o;
         o.flags = 0;
         o.src = 0;
         o.ri = o.rj = StepRec{0, 0, 0, 0};
-        const uint64_t q0 = unit * 32;
-        const uint64_t q = q0 + lane;
-        const bool active = q < a.steps;
+        const uint64_t q0 = static_cast<uint64_t>(unit) * 32;
+        const bool active = q0 + lane < a.steps;
         // batch boundaries count this warp's own steps (engine.cpp:115-124)
         uint32_t in_batch = b0 + lane;
         if (a.batch >= 32) {
@@ -127,20 +132,25 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const bool cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
         const uint32_t n_active = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
         carry = __shfl_sync(kFull, cooling, n_active - 1);  // batch still open after this unit
-        b0 = (b0 + n_active) % a.batch;
+        b0 += n_active;
+        if (a.batch >= 32) {  // b0 < batch and n_active <= 32: one subtraction
+            if (b0 >= a.batch) b0 -= a.batch;
+        } else {
+            b0 %= a.batch;
+        }
 
         // every lane loads its record, active or not: an in-tile partner of an
         // active lane may sit in an inactive lane of the last, partial unit
-        const uint64_t i0 = unit_i0;           // first step of the unit, q0 mod S (warp-uniform)
-        uint64_t gi = i0 + lane;
+        const UX i0 = unit_i0;                 // first step of the unit, q0 mod S (warp-uniform)
+        UX gi = i0 + lane;
         while (gi >= S) gi -= S;               // the unit wraps at the end of a pass (S < 32: repeatedly)
         uint32_t p = 0;
-        uint64_t pbase = 0;
-        int64_t n = 0;
+        UX pbase = 0;
+        SX n = 0;
         if (active) {
             p = path_of_step(g, gi);
-            pbase = __ldg(g.cum + p);
-            n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
+            pbase = static_cast<UX>(__ldg(g.cum + p));
+            n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + p + 1)) - pbase);
         }
         // Shared partner draws. Uniform batches (pair_window >= 1): lane 0
         // draws one position w0 on its path; every uniform lane on that path
@@ -172,15 +182,15 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         // path lookup so its DRAM latency is waited for only in next round's update
         o.ri = load_step_stream(g.step + gi, pol_stream);
         if (!active || n < 2) return o;
-        const int64_t i = static_cast<int64_t>(gi - pbase);
-        int64_t j;
+        const SX i = static_cast<SX>(gi - pbase);
+        SX j;
         uint64_t bits;
         if (cooling) {
             const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
             const uint64_t zt = __ldg(&g.pc[p].ztab);
-            const int64_t k = static_cast<int64_t>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
+            const SX k = static_cast<SX>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
             bits = r.next();
-            const int64_t sign = (shared ? (tag >> 31) : ((bits >> 61) & 1)) ? 1 : -1;
+            const SX sign = (shared ? (tag >> 31) : ((bits >> 61) & 1)) ? 1 : -1;
             j = i + sign * k;
             if (j < 0 || j >= n) {
                 j = i - sign * k;
@@ -192,20 +202,20 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             if (j == i) return o;
         } else {
             if (shared) {
-                const uint64_t w0 = __umul64hi(draw, static_cast<uint64_t>(n));
-                uint64_t jj = w0 + (lane ^ static_cast<uint32_t>(draw & 31));
-                if (jj >= static_cast<uint64_t>(n)) jj = n >= 32 ? jj - n : jj % n;
-                j = static_cast<int64_t>(jj);
+                const UX w0 = static_cast<UX>(__umul64hi(draw, static_cast<uint64_t>(n)));
+                UX jj = w0 + (lane ^ static_cast<uint32_t>(draw & 31));
+                if (jj >= static_cast<UX>(n)) jj = n >= 32 ? jj - n : jj % n;
+                j = static_cast<SX>(jj);
             } else {
-                j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+                j = static_cast<SX>(r.below(static_cast<uint64_t>(n)));
             }
             if (j == i) {
-                j = static_cast<int64_t>(r.below(static_cast<uint64_t>(n)));
+                j = static_cast<SX>(r.below(static_cast<uint64_t>(n)));
                 if (j == i) return o;
             }
             bits = r.next();
         }
-        const uint64_t gj = pbase + static_cast<uint64_t>(j);
+        const UX gj = pbase + static_cast<UX>(j);
         uint32_t fl = 1u | ((bits >> 63) ? 0u : 2u) | (((bits >> 62) & 1) ? 0u : 4u);
         if (gj >= i0 && gj - i0 < 32) {
             fl |= 8u;
@@ -248,29 +258,31 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 
     // i0 = 32u mod S, kept incrementally in spread order (no 64-bit division
     // per round): u advances by perm_step, or by perm_step - U on a wrap
-    uint64_t i0 = (u * 32) % S;
-    auto advance = [&](uint64_t& uu, uint64_t& ii) {
-        uu += a.perm_step;
+    UX i0 = static_cast<UX>((static_cast<uint64_t>(u) * 32) % g.total_steps);
+    const UX perm_step = static_cast<UX>(a.perm_step), i0_step = static_cast<UX>(a.i0_step),
+             i0_wrap = static_cast<UX>(a.i0_wrap);
+    auto advance = [&](UX& uu, UX& ii) {  // no overflow: uu, perm_step < U < 2^31; ii, i0_* < S < 2^31
+        uu += perm_step;
         if (uu >= U) {
             uu -= U;
-            ii += a.i0_wrap;
+            ii += i0_wrap;
         } else {
-            ii += a.i0_step;
+            ii += i0_step;
         }
         if (ii >= S) ii -= S;
     };
     if (kDepth == 2) {
         if (n_mine) {
             TileSel cur = select(u, i0);
-            for (uint64_t m = 0; m < n_mine; ++m) {
+            for (UX m = 0; m < n_mine; ++m) {
                 TileSel nxt;
                 nxt.flags = 0;
                 nxt.src = 0;
                 if (m + 1 < n_mine) {
                     k += a.n_warps;
                     if (a.fronts) {
-                        u = front_unit(k);
-                        i0 = (u * 32) % S;
+                        u = static_cast<UX>(front_unit(k));
+                        i0 = static_cast<UX>((static_cast<uint64_t>(u) * 32) % g.total_steps);
                     } else {
                         advance(u, i0);
                     }
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         // selection work of unit m+1 so the latter hides their latency
         if (n_mine) {
             TileSel cur = select(u, i0);
-            for (uint64_t m = 0; m < n_mine; ++m) {
+            for (UX m = 0; m < n_mine; ++m) {
                 StepRec sh;
                 sh.node = __shfl_sync(kFull, cur.ri.node, cur.src);
                 sh.ps_lo = __shfl_sync(kFull, cur.ri.ps_lo, cur.src);
@@ -331,9 +343,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
     } else if (n_mine) {
         // Stage A: the unit's record bytes into L2 (wrapping at the end of a pass)
-        auto prefetch_unit = [&](uint64_t uu, uint64_t ii) {
+        auto prefetch_unit = [&](UX uu, UX ii) {
             if (S < 32) return;  // warp-uniform arguments: one UBLKPF per warp
-            const uint64_t q0 = uu * 32;
+            const uint64_t q0 = static_cast<uint64_t>(uu) * 32;
             const uint32_t n_act = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
             const uint32_t first = static_cast<uint32_t>(S - ii < n_act ? S - ii : n_act);
             prefetch_bulk_l2(g.step + ii, first * static_cast<uint32_t>(sizeof(StepRec)));
@@ -352,7 +364,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 prefetch_l2_keep(coord_addr<T>(coords, o.rj.node, (o.flags >> 2) & 1));
             }
         };
-        uint64_t pu = u, pi = i0;  // prefetch cursor: one unit ahead of the select cursor
+        UX pu = u, pi = i0;  // prefetch cursor: one unit ahead of the select cursor
         prefetch_unit(pu, pi);
         for (int t = 1; t < 3 && t < static_cast<int>(n_mine); ++t) {
             advance(pu, pi);
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             advance(u, i0);
             nxt = select(u, i0);      // unit 1
         }
-        for (uint64_t m = 0; m < n_mine; ++m) {
+        for (UX m = 0; m < n_mine; ++m) {
             if (m + 3 < n_mine) {
                 advance(pu, pi);
                 prefetch_unit(pu, pi);
@@ -426,30 +438,44 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     flush_stat(stats, 7, b_second);
 }
 
-// variant 0 (default): two-stage; 1: two-stage, 3 CTAs/SM (80 registers);
-// 2: four-stage pipeline (no fronts order). Measured at configs 2 and 3 with
-// shared partner windows: the two-stage kernel matches or beats the
-// four-stage one, whose L2 prefetches no longer hide anything once partner
-// loads are coalesced.
+// Tile-kernel variants (pgl_layout_ext.kernel_variant; 0 = auto, chosen by
+// the host):
+//   1  two-stage pipeline, 2 CTAs/SM (no spills)
+//   2  two-stage pipeline, 3 CTAs/SM (80 registers)
+//   3  three-stage: endpoint loads of unit m issued before the selection of
+//      unit m+1, 3 CTAs/SM; the fastest at configs 2-3 (+5-7%), but its longer
+//      read-to-write window costs ~0.8% SPS where the concurrency cap binds
+//      (config 1), so auto picks it only when the graph fills the GPU
+//   4  four-stage pipeline with bulk L2 prefetch of records and endpoints
+// Bit 4 forces the 64-bit index instantiation (measurements).
+template <typename T, bool k32>
+const void* tiles_fn_t(int variant) {
+    return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 2, k32>)
+           : variant == 3 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 3, k32>)
+           : variant == 4 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 4, k32>)
+                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 2, k32>);
+}
+
 template <typename T>
-const void* tiles_fn(int variant) {
-    return variant == 1   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 2>)
-           : variant == 2 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 4>)
-           : variant == 3 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 3>)
-           : variant == 4 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 3>)
-                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 2>);
+const void* tiles_fn(int variant, bool k32) {
+    return k32 ? tiles_fn_t<T, true>(variant) : tiles_fn_t<T, false>(variant);
 }
 
 }  // namespace
 
-LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant) {
+LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant,
+                        uint64_t total_steps) {
     LaunchShape sh;
-    sh.threads = block_threads > 0 ? block_threads : 256;
+    // 32-bit index kernel when every signed step offset i +- k stays below 2^31
+    // (variant bit 4 forces the 64-bit instantiation, for measurements)
+    sh.idx32 = total_steps < (1ULL << 30) && !(variant & 16);
+    variant &= 15;
     sh.variant = variant;
+    sh.threads = block_threads > 0 ? block_threads : 256;
     int sms = 0, occ = 0;
     PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, coord_f64 ? tiles_fn<double>(variant) : tiles_fn<float>(variant), sh.threads, 0));
+        &occ, coord_f64 ? tiles_fn<double>(variant, sh.idx32) : tiles_fn<float>(variant, sh.idx32), sh.threads, 0));
     if (occ < 1) occ = 1;
     uint64_t warps = static_cast<uint64_t>(sms) * occ * (sh.threads / 32);
     if (max_warps && warps > max_warps) warps = max_warps;
@@ -461,7 +487,7 @@ LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block
 void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_f64, DevRng rng, DevStats* stats,
                       const IterArgs& a, LaunchShape shape, void* stream) {
     void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
-    PGL_CUDA(cudaLaunchKernel(coord_f64 ? tiles_fn<double>(shape.variant) : tiles_fn<float>(shape.variant),
+    PGL_CUDA(cudaLaunchKernel(coord_f64 ? tiles_fn<double>(shape.variant, shape.idx32) : tiles_fn<float>(shape.variant, shape.idx32),
                               dim3(shape.blocks), dim3(shape.threads), args, 0, static_cast<cudaStream_t>(stream)));
 }
 
