@@ -375,6 +375,10 @@ int pgl_layout_write_tsv(const char* path, const double* coords, uint64_t n_node
  * with pgl_free); same exception classes/messages, first failure in line
  * order. */
 int pgl_layout_read_tsv(const char* path, uint32_t threads, uint64_t* n_nodes, double** coords);
+/* In-memory forms (the reference's ostream/istream signatures): *text is a
+ * malloc'd, NUL-terminated buffer of *size bytes; free both with pgl_free. */
+int pgl_layout_format_tsv(const double* coords, uint64_t n_nodes, uint32_t threads, char** text, uint64_t* size);
+int pgl_layout_parse_tsv(const char* data, uint64_t size, uint32_t threads, uint64_t* n_nodes, double** coords);
 void pgl_free(void* p);
 
 /* ---- host-side helpers of the path (bit-exact with the reference) -------- */

@@ -89,6 +89,11 @@ inline void fail(const char* kind, const char* expr, const char* file, int line)
         }                                                                            \
         if (!dt_ok) doctest::detail::fail("CHECK_THROWS_AS", #expr ", " #T, __FILE__, __LINE__); \
     } while (0)
+#define FAIL(msg)                                                                    \
+    do {                                                                             \
+        doctest::detail::fail("FAIL", msg, __FILE__, __LINE__);                      \
+        throw doctest::detail::RequireFailed{};                                      \
+    } while (0)
 #define CHECK_NOTHROW(expr)                                                          \
     do {                                                                             \
         try {                                                                        \

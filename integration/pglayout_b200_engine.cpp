@@ -26,28 +26,13 @@
 
 #include "pglayout/engine.hpp"
 #include "pgl_b200.h"
+#include "pgl_facade_errors.hpp"
 
 namespace pglayout {
 
 namespace {
 
-[[noreturn]] void rethrow(int rc) {
-    const std::string msg = pgl_last_error();
-    // strip the "TypeName: " prefix; the reference constructors add it back
-    const std::string detail = msg.find(": ") != std::string::npos ? msg.substr(msg.find(": ") + 2) : msg;
-    switch (pgl_last_error_type()) {
-        case PGL_ERR_INVALID_PARAMETER: throw InvalidParameter(detail);
-        case PGL_ERR_UNKNOWN_NODE: throw UnknownNode(detail);
-        case PGL_ERR_EMPTY_PATH: throw EmptyPath(detail);
-        case PGL_ERR_INDEX_OUT_OF_RANGE: throw IndexOutOfRange(detail);
-        case PGL_ERR_EMPTY_GRAPH: throw EmptyGraph(detail);
-        case PGL_ERR_DEGENERATE_GRAPH: throw DegenerateGraph(detail);
-        case PGL_ERR_ZERO_REFERENCE: throw ZeroReference(detail);
-        default: break;
-    }
-    throw Error(rc == PGL_E_USAGE ? ErrorKind::usage : rc == PGL_E_INPUT ? ErrorKind::input : ErrorKind::internal,
-                msg);
-}
+using b200::rethrow;
 
 pgl_layout_config to_c(const LayoutConfig& c) {
     pgl_layout_config o;

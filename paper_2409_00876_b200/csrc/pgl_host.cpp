@@ -1157,6 +1157,35 @@ int pgl_layout_read_tsv(const char* path, uint32_t threads, uint64_t* n_nodes, d
     });
 }
 
+int pgl_layout_format_tsv(const double* coords, uint64_t n_nodes, uint32_t threads, char** text, uint64_t* size) {
+    return guarded([&] {
+        if ((!coords && n_nodes) || !text || !size) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *text = nullptr;
+        *size = 0;
+        const std::string t = layout_format_tsv(coords, n_nodes, threads);
+        char* m = static_cast<char*>(std::malloc(t.size() + 1));
+        if (!m) throw std::bad_alloc();
+        std::memcpy(m, t.data(), t.size());
+        m[t.size()] = 0;
+        *text = m;
+        *size = t.size();
+    });
+}
+
+int pgl_layout_parse_tsv(const char* data, uint64_t size, uint32_t threads, uint64_t* n_nodes, double** coords) {
+    return guarded([&] {
+        if ((!data && size) || !n_nodes || !coords) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *coords = nullptr;
+        *n_nodes = 0;
+        std::vector<double> v = layout_read_tsv_buffer(data ? data : "", size, threads);
+        double* m = static_cast<double*>(std::malloc(std::max<size_t>(v.size(), 1) * sizeof(double)));
+        if (!m) throw std::bad_alloc();
+        std::memcpy(m, v.data(), v.size() * sizeof(double));
+        *coords = m;
+        *n_nodes = v.size() / 4;
+    });
+}
+
 void pgl_free(void* p) { std::free(p); }
 
 int pgl_make_schedule(const pgl_graph_view* v, const pgl_layout_config* cfg, double* etas) {

@@ -168,7 +168,9 @@ const char* gfa_path_name(const GfaGraph* g, uint32_t p);
 
 // Layout table IO (pgl_tsv.cpp).
 void layout_write_tsv(const char* path, const double* coords, uint64_t n_nodes, uint32_t threads);
+std::string layout_format_tsv(const double* coords, uint64_t n_nodes, uint32_t threads);
 std::vector<double> layout_read_tsv(const char* path, uint32_t threads);
+std::vector<double> layout_read_tsv_buffer(const char* data, uint64_t size, uint32_t threads);
 
 // Small device helpers used by the host driver.
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);

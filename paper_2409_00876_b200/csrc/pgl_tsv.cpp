@@ -54,7 +54,18 @@ unsigned threads_for(uint32_t threads, uint64_t work, uint64_t grain) {
 
 }  // namespace
 
+std::string layout_format_tsv(const double* c, uint64_t n, uint32_t threads);
+
 void layout_write_tsv(const char* path, const double* c, uint64_t n, uint32_t threads) {
+    const std::string text = layout_format_tsv(c, n, threads);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) raise(PGL_ERR_INVALID_PARAMETER, std::string("cannot write '") + path + "'");
+    bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) raise(PGL_ERR_INVALID_PARAMETER, std::string("short write to '") + path + "'");
+}
+
+std::string layout_format_tsv(const double* c, uint64_t n, uint32_t threads) {
     const unsigned T = threads_for(threads, n, 1 << 16);
     // non-finite check first: the lowest offending node (layout_io.cpp:37-40)
     std::atomic<uint64_t> bad{kNoLine};
@@ -87,12 +98,14 @@ void layout_write_tsv(const char* path, const double* c, uint64_t n, uint32_t th
             }
         }
     });
-    FILE* f = std::fopen(path, "wb");
-    if (!f) raise(PGL_ERR_INVALID_PARAMETER, std::string("cannot write '") + path + "'");
-    bool ok = std::fwrite(kHeader.data(), 1, kHeader.size(), f) == kHeader.size() && std::fputc('\n', f) != EOF;
-    for (const auto& s : blocks) ok = ok && std::fwrite(s.data(), 1, s.size(), f) == s.size();
-    ok = (std::fclose(f) == 0) && ok;
-    if (!ok) raise(PGL_ERR_INVALID_PARAMETER, std::string("short write to '") + path + "'");
+    uint64_t total = kHeader.size() + 1;
+    for (const auto& b : blocks) total += b.size();
+    std::string text;
+    text.reserve(total);
+    text.append(kHeader.data(), kHeader.size());
+    text.push_back('\n');
+    for (const auto& b : blocks) text.append(b);
+    return text;
 }
 
 namespace {

@@ -25,7 +25,7 @@ def run(name, timeout=900):
     return p
 
 
-@pytest.mark.parametrize("suite", ["test_engine", "test_metrics", "test_rng", "test_graph"])
+@pytest.mark.parametrize("suite", ["test_engine", "test_metrics", "test_rng", "test_graph", "test_gfa_io"])
 def test_reference_unit_suite_passes_on_b200_facade(gpu, suite):
     p = run(suite)
     assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
