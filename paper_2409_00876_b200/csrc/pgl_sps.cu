@@ -206,9 +206,3 @@ void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64, uint6
 }
 
 }  // namespace pgl
-
-namespace pgl {
-void run_sps_stream(const DevGraph&, const void*, int, uint64_t, uint32_t, pgl_stress_report*, double*, void*) {
-    raise(PGL_ERR_INVALID_PARAMETER, "PGL_SPS_STREAM is not available in this build");
-}
-}  // namespace pgl

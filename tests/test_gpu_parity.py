@@ -339,3 +339,40 @@ def test_hogwild_sps_parity_config1(pgl, oracle, ref, gpu, samp):
         cpu_sps.append(ref.sps(gr, lay, 7, 100).mean)
     ratio = np.median(gpu_sps) / np.median(cpu_sps)
     assert 0.98 <= ratio <= 1.02, (gpu_sps, cpu_sps, ratio)
+
+
+# ---- PGL_SPS_STREAM: the reference's own sampled-stress stream on the device --------
+
+STREAM_CASES = [(SMALL[0], 7, 100), (SMALL[1], 123, 10), (SMALL[2], 5, 1), ((2, 20, 1, 0.0), 11, 100),
+                ((4, 2, 3, 0.0), 3, 50), (C1, 7, 100)]
+
+
+@pytest.mark.parametrize("args,seed,spn", STREAM_CASES)
+def test_sps_stream_replays_reference(pgl, ref, gpu, args, seed, spn):
+    """Same terms as metrics.cpp:108-159 (n and skipped identical), mean and
+    sigma equal up to summation order (the reference's own contract,
+    test_metrics.cpp:273-289, allows 1e-12)."""
+    g = pgl.generate_synthetic_pangenome(*args)
+    gr = ref.generate(*args)
+    for lay in (ref.init_layout(gr, 3), pgl.run_layout(g, pgl.LayoutConfig(global_seed=seed, n_iters=5))):
+        got = pgl.sampled_path_stress(g, lay, seed, spn, method=pgl.SPS_STREAM)
+        want = ref.sps(gr, lay, seed, spn)
+        assert (got.n, got.skipped) == (want.n, want.skipped)
+        assert got.mean == pytest.approx(want.mean, rel=1e-12, abs=1e-300)
+        assert got.std_dev == pytest.approx(want.std_dev, rel=1e-10, abs=1e-300)
+        assert got.ci_low == pytest.approx(want.ci_low, rel=1e-10, abs=1e-300)
+
+
+def test_sps_stream_revisits(pgl, oracle, ref, gpu):
+    """Abutting steps and revisits: degenerate coin pairs and skipped samples."""
+    g, go = revisit_graph(pgl, oracle)
+    lens = [5, 3, 7, 2, 9, 4]
+    walks = [[(0, 0), (1, 1), (2, 0), (1, 0), (3, 1), (0, 0), (4, 0)],
+             [(5, 1), (2, 1), (2, 1), (3, 0), (4, 1)],
+             [(1, 0)]]
+    gr = ref.build(lens, walks)
+    lay = pgl.init_layout(g, 9)
+    got = pgl.sampled_path_stress(g, lay, 17, 200, method=pgl.SPS_STREAM)
+    want = ref.sps(gr, lay, 17, 200)
+    assert (got.n, got.skipped) == (want.n, want.skipped)
+    assert got.mean == pytest.approx(want.mean, rel=1e-12)
