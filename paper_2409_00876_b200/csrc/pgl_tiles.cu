@@ -37,7 +37,6 @@ namespace pgl {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr uint32_t kSmemPaths = 1024;  // paths whose constants live in shared memory
 
 __device__ __forceinline__ void flush_stat(DevStats* st, int idx, uint32_t v) {
     const uint32_t sum = __reduce_add_sync(kFull, v);
@@ -78,20 +77,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint32_t warp = static_cast<uint32_t>(tid >> 5);
     const uint32_t lane = threadIdx.x & 31;
-    // per-path constants in shared memory when they fit: the path of a step
-    // is a short binary search over cum (short-scoreboard loads that never
-    // wait behind the global gathers in flight), Zipf support + table offset
-    __shared__ uint64_t s_cum[kSmemPaths + 1];
-    __shared__ uint2 s_zip[kSmemPaths];
-    const uint32_t P = g.n_paths;
-    const bool smem_paths = P <= kSmemPaths;
-    if (smem_paths) {
-        for (uint32_t k = threadIdx.x; k <= P; k += blockDim.x) {
-            s_cum[k] = g.cum[k];
-            if (k < P) s_zip[k] = make_uint2(static_cast<uint32_t>(g.pc[k].zn), static_cast<uint32_t>(g.pc[k].ztab));
-        }
-    }
-    __syncthreads();
     if (warp >= a.n_warps) return;
 
     Xo r{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
@@ -163,23 +148,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         UX pbase = 0;
         SX n = 0;
         if (active) {
-            if (smem_paths) {
-                uint32_t lo = 0, hi = P;  // largest p with cum[p] <= gi
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (s_cum[mid] <= gi)
-                        lo = mid;
-                    else
-                        hi = mid;
-                }
-                p = lo;
-                pbase = static_cast<UX>(s_cum[p]);
-                n = static_cast<SX>(static_cast<UX>(s_cum[p + 1]) - pbase);
-            } else {
-                p = path_of_step(g, gi);
-                pbase = static_cast<UX>(__ldg(g.cum + p));
-                n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + p + 1)) - pbase);
-            }
+            p = path_of_step(g, gi);
+            pbase = static_cast<UX>(__ldg(g.cum + p));
+            n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + p + 1)) - pbase);
         }
         // Shared partner draws. Uniform batches (pair_window >= 1): lane 0
         // draws one position w0 on its path; every uniform lane on that path
@@ -215,16 +186,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         SX j;
         uint64_t bits;
         if (cooling) {
-            uint32_t zn;
-            uint64_t zt;
-            if (smem_paths) {
-                const uint2 z = s_zip[p];
-                zn = z.x;
-                zt = z.y;
-            } else {
-                zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
-                zt = __ldg(&g.pc[p].ztab);
-            }
+            const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
+            const uint64_t zt = __ldg(&g.pc[p].ztab);
             const SX k = static_cast<SX>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
             bits = r.next();
             const SX sign = (shared ? (tag >> 31) : ((bits >> 61) & 1)) ? 1 : -1;
