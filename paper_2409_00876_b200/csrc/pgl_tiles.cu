@@ -102,7 +102,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     uint32_t b0 = 0;  // this warp's step count mod batch (batch boundaries, engine.cpp:115-124)
 
     // Stage A: batch decision, i's record (coalesced), partner selection.
-    auto select = [&](UX unit, UX unit_i0) -> TileSel {
+    // path of the lane's step in a unit (sguide + cum, L1-resident)
+    struct Loc {
+        uint32_t p;
+        UX pbase;
+        SX n;
+    };
+    auto locate = [&](UX unit, UX unit_i0) -> Loc {
+        Loc l{0, 0, 0};
+        if (static_cast<uint64_t>(unit) * 32 + lane < a.steps) {
+            UX gi = unit_i0 + lane;
+            while (gi >= S) gi -= S;
+            l.p = path_of_step(g, gi);
+            l.pbase = static_cast<UX>(__ldg(g.cum + l.p));
+            l.n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + l.p + 1)) - l.pbase);
+        }
+        return l;
+    };
+    auto select = [&](UX unit, UX unit_i0, const Loc* pre) -> TileSel {
         TileSel o;
         o.flags = 0;
         o.src = 0;
@@ -147,7 +164,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         uint32_t p = 0;
         UX pbase = 0;
         SX n = 0;
-        if (active) {
+        if (pre) {
+            p = pre->p;
+            pbase = pre->pbase;
+            n = pre->n;
+        } else if (active) {
             p = path_of_step(g, gi);
             pbase = static_cast<UX>(__ldg(g.cum + p));
             n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + p + 1)) - pbase);
@@ -273,7 +294,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     };
     if (kDepth == 2) {
         if (n_mine) {
-            TileSel cur = select(u, i0);
+            TileSel cur = select(u, i0, nullptr);
             for (UX m = 0; m < n_mine; ++m) {
                 TileSel nxt;
                 nxt.flags = 0;
@@ -286,7 +307,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     } else {
                         advance(u, i0);
                     }
-                    nxt = select(u, i0);
+                    nxt = select(u, i0, nullptr);
                 }
                 applied += update(cur);
                 cur = nxt;
@@ -296,8 +317,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         // two-stage, with the endpoint loads of unit m issued before the
         // selection work of unit m+1 so the latter hides their latency
         if (n_mine) {
-            TileSel cur = select(u, i0);
+            TileSel cur = select(u, i0, nullptr);
             for (UX m = 0; m < n_mine; ++m) {
+                // the next unit's path lookup first: its (L1) loads must not
+                // share a scoreboard with the endpoint gathers issued below
+                Loc nloc{0, 0, 0};
+                UX nu = u, ni0 = i0;
+                if (m + 1 < n_mine) {
+                    advance(nu, ni0);
+                    nloc = locate(nu, ni0);
+                }
                 StepRec sh;
                 sh.node = __shfl_sync(kFull, cur.ri.node, cur.src);
                 sh.ps_lo = __shfl_sync(kFull, cur.ri.ps_lo, cur.src);
@@ -317,8 +346,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 nxt.flags = 0;
                 nxt.src = 0;
                 if (m + 1 < n_mine) {
-                    advance(u, i0);
-                    nxt = select(u, i0);
+                    u = nu;
+                    i0 = ni0;
+                    nxt = select(u, i0, &nloc);
                 }
                 if ((cur.flags & 1u) && d_ref > 0.0)
                     applied += hog_apply_t<T>(coords, cur.ri.node, ei, cur.rj.node, ej, d_ref, a.eta, r, pol_keep,
@@ -370,14 +400,14 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             advance(pu, pi);
             prefetch_unit(pu, pi);
         }
-        TileSel cur = select(u, i0);  // unit 0
+        TileSel cur = select(u, i0, nullptr);  // unit 0
         resolve(cur);
         TileSel nxt;
         nxt.flags = 0;
         nxt.src = 0;
         if (n_mine > 1) {
             advance(u, i0);
-            nxt = select(u, i0);      // unit 1
+            nxt = select(u, i0, nullptr);      // unit 1
         }
         for (UX m = 0; m < n_mine; ++m) {
             if (m + 3 < n_mine) {
@@ -400,7 +430,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             nn.src = 0;
             if (m + 2 < n_mine) {
                 advance(u, i0);
-                nn = select(u, i0);   // stage B, unit m+2
+                nn = select(u, i0, nullptr);   // stage B, unit m+2
             }
             if (m + 1 < n_mine) resolve(nxt);  // stage C, unit m+1
             // Stage D arithmetic + write-back for unit m
