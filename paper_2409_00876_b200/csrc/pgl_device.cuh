@@ -260,6 +260,24 @@ __device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) 
 __device__ __forceinline__ void prefetch_l2_keep(const void* p) {
     asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(p));
 }
+// Asynchronous global -> shared copies (LDGSTS), completion tracked per
+// thread by commit/wait groups: the loads hold no registers while in flight.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+template <int kBytes>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc, uint64_t pol) {
+    if constexpr (kBytes == 16)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                     :: "r"(smem_u32(smem_dst)), "l"(gsrc), "l"(pol) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;"
+                     :: "r"(smem_u32(smem_dst)), "l"(gsrc), "n"(kBytes), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
 template <typename T>
 __device__ __forceinline__ const void* coord_addr(const void* base, uint32_t node, int end) {
     return reinterpret_cast<const char*>(base) + (2 * static_cast<uint64_t>(node) + end) * (2 * sizeof(T));

@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
         return l;
     };
+    StepRec* async_ri = nullptr;  // kDepth 5: shared-memory destinations of select's record copies
+    StepRec* async_rj = nullptr;
     auto select = [&](UX unit, UX unit_i0, const Loc* pre) -> TileSel {
         TileSel o;
         o.flags = 0;
@@ -201,7 +203,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const bool shared = ((tag >> 30) & 1) && ((tag >> 29) & 1) == (cooling ? 1u : 0u) && (tag & 0x1FFFFFFFu) == p;
         // the unit's records (one coalesced 512-byte load), issued after the
         // path lookup so its DRAM latency is waited for only in next round's update
-        o.ri = load_step_stream(g.step + gi, pol_stream);
+        if constexpr (kDepth == 5)
+            cp_async<16>(async_ri + lane, g.step + gi, pol_stream);
+        else
+            o.ri = load_step_stream(g.step + gi, pol_stream);
         if (!active || n < 2) return o;
         const SX i = static_cast<SX>(gi - pbase);
         SX j;
@@ -242,7 +247,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             fl |= 8u;
             o.src = static_cast<uint32_t>(gj - i0);
         } else {
-            o.rj = load_step_stream(g.step + gj, pol_stream);
+            if constexpr (kDepth == 5)
+                cp_async<16>(async_rj + lane, g.step + gj, pol_stream);
+            else
+                o.rj = load_step_stream(g.step + gj, pol_stream);
         }
         o.flags = fl;
         return o;
@@ -311,6 +319,103 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 }
                 applied += update(cur);
                 cur = nxt;
+            }
+        }
+    } else if (kDepth == 5) {
+        // Asynchronous pipeline: records and endpoints travel global ->
+        // shared by cp.async (no registers held while in flight). Round m:
+        //   1. wait for the endpoints of unit m, apply its update;
+        //   2. wait for the records of unit m+1, resolve its partner (own
+        //      copy, or the in-tile owner's slot), issue its endpoint copies;
+        //   3. select unit m+2, issue its record copies.
+        // Commit order ..., C(m), R(m+1), C(m+1), R(m+2): "wait_group 1"
+        // leaves only the newest group in flight.
+        using T2 = std::conditional_t<std::is_same_v<T, double>, double2, float2>;
+        constexpr int kWarps = 8;  // 256-thread blocks
+        __shared__ StepRec s_ri[3][kWarps][32], s_rj[3][kWarps][32];
+        __shared__ T2 s_vi[2][kWarps][32], s_vj[2][kWarps][32];
+        const int wib = static_cast<int>(threadIdx.x >> 5);
+        struct Res {  // a resolved update, waiting for its endpoints
+            uint32_t ni, nj, flags;
+            double d_ref;
+        };
+        auto issue_sel = [&](UX m, UX uu, UX ii) -> uint32_t {
+            async_ri = s_ri[m % 3][wib];
+            async_rj = s_rj[m % 3][wib];
+            const TileSel t = select(uu, ii, nullptr);
+            cp_async_commit();
+            return t.flags | (t.src << 8);
+        };
+        auto resolve_issue = [&](UX m, uint32_t fs) -> Res {
+            Res rs{0, 0, 0, 0.0};
+            if (fs & 1u) {
+                const StepRec ri = s_ri[m % 3][wib][lane];
+                const StepRec rj = (fs & 8u) ? s_ri[m % 3][wib][fs >> 8] : s_rj[m % 3][wib][lane];
+                const int ei = (fs >> 1) & 1, ej = (fs >> 2) & 1;
+                rs.d_ref = abs_diff(step_pos(ri, ei), step_pos(rj, ej));
+                rs.ni = ri.node;
+                rs.nj = rj.node;
+                rs.flags = fs;
+                if (rs.d_ref > 0.0) {
+                    cp_async<sizeof(T2)>(&s_vi[m & 1][wib][lane], coord_addr<T>(coords, ri.node, ei), pol_keep);
+                    cp_async<sizeof(T2)>(&s_vj[m & 1][wib][lane], coord_addr<T>(coords, rj.node, ej), pol_keep);
+                }
+            }
+            cp_async_commit();
+            return rs;
+        };
+        if (n_mine) {
+            uint32_t f_next = issue_sel(0, u, i0);  // R(0)
+            cp_async_wait<0>();
+            __syncwarp();
+            Res cur = resolve_issue(0, f_next);     // C(0)
+            f_next = 0;
+            if (n_mine > 1) {
+                advance(u, i0);
+                f_next = issue_sel(1, u, i0);       // R(1)
+            } else {
+                cp_async_commit();
+            }
+            for (UX m = 0; m < n_mine; ++m) {
+                cp_async_wait<1>();                 // C(m) landed (R(m+1) may be in flight)
+                if ((cur.flags & 1u) && cur.d_ref > 0.0) {
+                    const T2 vi = s_vi[m & 1][wib][lane], vj = s_vj[m & 1][wib][lane];
+                    applied += hog_apply_t<T>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj, (cur.flags >> 2) & 1,
+                                              cur.d_ref, a.eta, r, pol_keep, vi.x, vi.y, vj.x, vj.y);
+                }
+                if ((cur.flags & 1u) && a.drf > 1) {
+                    const StepRec ri = s_ri[m % 3][wib][lane];
+                    const StepRec rj =
+                        (cur.flags & 8u) ? s_ri[m % 3][wib][cur.flags >> 8] : s_rj[m % 3][wib][lane];
+                    const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
+                    unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+                    for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                        int ea, eb;
+                        do {
+                            const uint64_t b2 = r.next();
+                            ea = (b2 >> 63) ? 0 : 1;
+                            eb = ((b2 >> 62) & 1) ? 0 : 1;
+                        } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                        used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                        applied += hog_update_t<T>(coords, ri.node, ea, rj.node, eb,
+                                                   abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, r, pol_keep);
+                    }
+                }
+                Res nres{0, 0, 0, 0.0};
+                if (m + 1 < n_mine) {
+                    cp_async_wait<0>();             // R(m+1) landed
+                    __syncwarp();                   // in-tile partners read other lanes' copies
+                    nres = resolve_issue(m + 1, f_next);  // C(m+1)
+                    f_next = 0;
+                    if (m + 2 < n_mine) {
+                        advance(u, i0);
+                        f_next = issue_sel(m + 2, u, i0);  // R(m+2)
+                    } else {
+                        cp_async_commit();
+                    }
+                }
+                __syncwarp();  // slot reuse: every lane is done with unit m's shared data
+                cur = nres;
             }
         }
     } else if (kDepth == 3) {
@@ -483,6 +588,8 @@ const void* tiles_fn_t(int variant) {
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 2, k32>)
            : variant == 3 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 3, k32>)
            : variant == 4 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 4, k32>)
+           : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 5, k32>)
+           : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 5, k32>)
                           : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 2, k32>);
 }
 
