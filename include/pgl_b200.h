@@ -159,7 +159,8 @@ typedef struct pgl_layout_ext {
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
     uint32_t kernel_variant;  /* tile kernel: 0 = auto; 1 = two-stage pipeline, 2 CTAs/SM;
                                  2 = two-stage, 3 CTAs/SM; 3 = three-stage (early endpoint
-                                 loads), 3 CTAs/SM; 4 = four-stage with L2 prefetch.
+                                 loads), 3 CTAs/SM; 4 = four-stage with L2 prefetch;
+                                 5/6 = cp.async pipeline via shared memory, 4/3 CTAs/SM.
                                  i.i.d. kernel: 0 = 2 CTAs/SM, 1 = 3 CTAs/SM */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
     uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */

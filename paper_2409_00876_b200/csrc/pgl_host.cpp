@@ -493,18 +493,18 @@ uint64_t next_prime(uint64_t n) {
     }
 }
 
-// Tile-kernel variant (pgl_tiles.cu): auto = the three-stage kernel at 3
-// CTAs/SM once the concurrency cap no longer binds (the graph fills the
-// GPU), else the two-stage kernel, whose shorter read-to-write window keeps
-// small graphs' layouts closest to the reference. The fronts order runs on
-// the two-stage kernel only.
+// Tile-kernel variant (pgl_tiles.cu): auto = the asynchronous cp.async
+// pipeline at 3 CTAs/SM once the concurrency cap no longer binds (the graph
+// fills the GPU), else the two-stage kernel, whose shorter read-to-write
+// window keeps small graphs' layouts closest to the reference. The fronts
+// order runs on the two-stage kernel only.
 int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
     int v = static_cast<int>(ext.kernel_variant & 15);
     const int force64 = static_cast<int>(ext.kernel_variant & 16);
     if (v == 0) {
         int sms = 0;
         PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        v = cap >= static_cast<uint32_t>(sms) * 3 * 8 ? 3 : 1;
+        v = cap >= static_cast<uint32_t>(sms) * 3 * 8 ? 6 : 1;
     }
     if (ext.unit_order == PGL_ORDER_FRONTS && v > 2) v = 1;
     return v | force64;

@@ -575,13 +575,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 
 // Tile-kernel variants (pgl_layout_ext.kernel_variant; 0 = auto, chosen by
 // the host):
-//   1  two-stage pipeline, 2 CTAs/SM (no spills)
+//   1  two-stage pipeline, 2 CTAs/SM (no spills); auto where the concurrency
+//      cap binds (small graphs: the shortest read-to-write window)
 //   2  two-stage pipeline, 3 CTAs/SM (80 registers)
 //   3  three-stage: endpoint loads of unit m issued before the selection of
-//      unit m+1, 3 CTAs/SM; the fastest at configs 2-3 (+5-7%), but its longer
-//      read-to-write window costs ~0.8% SPS where the concurrency cap binds
-//      (config 1), so auto picks it only when the graph fills the GPU
+//      unit m+1, 3 CTAs/SM
 //   4  four-stage pipeline with bulk L2 prefetch of records and endpoints
+//   5  asynchronous pipeline (cp.async records and endpoints staged in shared
+//      memory), 4 CTAs/SM (64 registers)
+//   6  the same at 3 CTAs/SM; auto once the graph fills the GPU (configs 2-5:
+//      C2 43 G upd/s vs 39-41 for variants 1/3)
 // Bit 4 forces the 64-bit index instantiation (measurements).
 template <typename T, bool k32>
 const void* tiles_fn_t(int variant) {
