@@ -191,23 +191,84 @@ void init_layout(const pgl_graph_view* v, uint64_t total_nt, uint64_t seed, doub
     }
 }
 
+// Device buffers come from the device's stream-ordered memory pool on the
+// owning graph's stream; the pool keeps up to kPoolKeep bytes reserved after
+// a graph is destroyed, so repeated layouts (pgl_layout_run per call) do not
+// pay cudaMalloc/cudaFree of their 1-15 GB index every time.
+constexpr uint64_t kPoolKeep = 48ULL << 30;
+
+void keep_pool(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done.push_back(device);
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s = nullptr;  // allocation / free stream (the owning graph's)
     void alloc(size_t count) {
         if (count <= n && p) return;
         release();
-        PGL_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+        PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(1, count) * sizeof(T), s));
         n = count;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
     }
     ~DevBuf() { release(); }
 };
+
+// Pinned staging blocks are recycled through a small process-wide pool
+// (cudaHostAlloc/cudaFreeHost of 128 MiB cost tens of milliseconds).
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<std::pair<void*, size_t>> free;
+    size_t held = 0;
+    static constexpr size_t kCap = 1ULL << 30;
+    void* get(size_t b, size_t* got) {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            for (size_t k = 0; k < free.size(); ++k)
+                if (free[k].second >= b) {
+                    void* p = free[k].first;
+                    *got = free[k].second;
+                    held -= *got;
+                    free.erase(free.begin() + static_cast<long>(k));
+                    return p;
+                }
+        }
+        void* p = nullptr;
+        PGL_CUDA(cudaHostAlloc(&p, b, cudaHostAllocDefault));
+        *got = b;
+        return p;
+    }
+    void put(void* p, size_t b) {
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            if (held + b <= kCap) {
+                free.emplace_back(p, b);
+                held += b;
+                return;
+            }
+        }
+        cudaFreeHost(p);
+    }
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* pool = new PinnedPool;  // leaked: outlives static destructors
+    return *pool;
+}
 
 struct PinnedBuf {
     void* p = nullptr;
@@ -215,11 +276,10 @@ struct PinnedBuf {
     void alloc(size_t b) {
         if (b <= bytes && p) return;
         release();
-        PGL_CUDA(cudaHostAlloc(&p, b, cudaHostAllocDefault));
-        bytes = b;
+        p = pinned_pool().get(b, &bytes);
     }
     void release() {
-        if (p) cudaFreeHost(p);
+        if (p) pinned_pool().put(p, bytes);
         p = nullptr;
         bytes = 0;
     }
@@ -339,11 +399,35 @@ struct pgl_graph {
     pgl_timing timing{};
     PinnedBuf pin;
 
+    void set_stream(cudaStream_t st) {
+        stream = st;
+        step.s = cum.s = stream;
+        guide.s = sguide.s = stream;
+        pc.s = stream;
+        zalias.s = stream;
+        coords64.s = stream;
+        coords32.s = stream;
+        rng.s = stream;
+        stats.s = stream;
+    }
     ~pgl_graph() {
         if (sps.part) cudaFree(sps.part);
         if (sps.cnt) cudaFree(sps.cnt);
         if (sps.scal) cudaFree(sps.scal);
-        if (stream) cudaStreamDestroy(stream);
+        step.release();
+        cum.release();
+        guide.release();
+        sguide.release();
+        pc.release();
+        zalias.release();
+        coords64.release();
+        coords32.release();
+        rng.release();
+        stats.release();
+        if (stream) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
     }
 
     DevGraph dev() const {
@@ -456,7 +540,10 @@ pgl_graph* create_graph(int device, const pgl_graph_view* v) {
     DeviceGuard dg(device);
     auto G = std::make_unique<pgl_graph>();
     G->device = device;
-    PGL_CUDA(cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking));
+    keep_pool(device);
+    cudaStream_t st;
+    PGL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    G->set_stream(st);
     G->n_nodes = v->n_nodes;
     G->n_paths = v->n_paths;
     G->sum = s;
