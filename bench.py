@@ -52,13 +52,23 @@ CONFIGS = {
     "c1": (1, 9680, 8, 0.05),
     "c2": (1, 968000, 90, 0.05),
     "c3": (1, 9680000, 90, 0.05),
+    "c5": (5, 200000, 500, 3, 0.05),  # generate_nested_pangenome(seed, backbone, paths, depth, site rate)
 }
 WORKLOAD_NAME = {
     "c1": "config 1: synthetic ~10k-node 8-path graph (generate_synthetic_pangenome(1, 9680, 8, 0.05)), 30 iters",
     "c2": "config 2: synthetic 1M-node 90-path graph (generate_synthetic_pangenome(1, 968000, 90, 0.05)), 30 iters",
     "c3": "config 3: chr1-scale synthetic 10M-node 90-path graph (generate_synthetic_pangenome(1, 9680000, 90, 0.05)), 30 iters",
+    "c5": ("config 5: high-complexity synthetic graph, nested bubbles (depth 3), inversions, duplications, "
+           "500 paths, zipf_space_max 1e5 (generate_nested_pangenome(5, 200000, 500, 3, 0.05)), 30 iters"),
 }
 FALLBACK_HBM_GBS = 6650.0
+CONFIG_LAYOUT = {"c5": {"zipf_space_max": 100000}}  # LayoutConfig overrides per config
+
+
+def make_graph(P, config):
+    if config == "c5":
+        return P.generate_nested_pangenome(*CONFIGS[config])
+    return P.generate_synthetic_pangenome(*CONFIGS[config])
 
 
 def parse():
@@ -212,15 +222,21 @@ def cpu_reference_sample(args, n_steps_total=1, budget_s=20.0):
     if not os.path.exists(REF_SO):
         return None
     R = Reference()
-    seed, bb, paths, rate = CONFIGS[args.config]
-    g = R.generate(seed, bb, paths, rate, gfa_roundtrip=(args.config == "c1"))
+    if args.config == "c5":  # the fixture's walks, built by the reference's own build_graph
+        import paper_2409_00876_b200 as P
+        gp = make_graph(P, "c5")
+        g = R.build(gp.node_len.tolist(),
+                    [list(zip(s["node_id"].tolist(), s["orient"].tolist())) for s in gp.path_steps])
+        del gp
+    else:
+        g = R.generate(*CONFIGS[args.config], gfa_roundtrip=(args.config == "c1"))
     cores = os.cpu_count() or 1
     # ~1.5 M updates/s per core measured for the reference at this scale
     est_rate = 1.5e6 * cores
     per_iter_full = 10 * g.total_steps
     want = max(est_rate * budget_s / 2.0, 2e6)
     srf = max(1, int(math.ceil(per_iter_full / want)))
-    cfg = make_cfg(n_iters=2, threads=cores, srf=srf, global_seed=101)
+    cfg = make_cfg(n_iters=2, threads=cores, srf=srf, global_seed=101, **CONFIG_LAYOUT.get(args.config, {}))
     rates = []
     sample = None
     for _ in range(n_steps_total):
@@ -245,7 +261,6 @@ def run_reference_arm(args, dist: Dist):
     _, cores, sample, kind, rates = res
     timed = rates[args.warmup:] or rates
     v = statistics.median(timed)
-    seed, bb, paths, rate = CONFIGS[args.config]
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
@@ -266,10 +281,9 @@ def run_ours(args, dist: Dist):
     torch.cuda.set_device(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
 
-    seed, bb, paths, rate = CONFIGS[args.config]
-    g = P.generate_synthetic_pangenome(seed, bb, paths, rate)
+    g = make_graph(P, args.config)
     S = g.total_steps()
-    cfg = P.LayoutConfig(global_seed=42 + dist.rank)
+    cfg = P.LayoutConfig(global_seed=42 + dist.rank, **CONFIG_LAYOUT.get(args.config, {}))
     ext = P.LayoutExt(coord_precision=P.COORD_F64 if args.coord == "f64" else P.COORD_F32)
     updates = cfg.n_iters * (10 * S // cfg.srf) * cfg.drf
 

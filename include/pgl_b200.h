@@ -412,6 +412,13 @@ typedef struct pgl_synthetic pgl_synthetic;
 int pgl_synthetic_generate(uint64_t seed, uint64_t backbone_nodes,
                            uint32_t n_paths, double variant_rate,
                            pgl_synthetic** out);
+/* Config 5 fixture (not in the reference): nested bubbles up to `depth`
+ * levels (substitution branches with their own sites), inversions (reverse
+ * steps), deletions and duplications (node revisits), `site_rate` sites per
+ * backbone node, per-path allele choices. Deterministic in its arguments;
+ * its walks are plain build_graph input. */
+int pgl_synthetic_generate_nested(uint64_t seed, uint64_t backbone_nodes, uint32_t n_paths,
+                                  uint32_t depth, double site_rate, pgl_synthetic** out);
 int pgl_synthetic_view(const pgl_synthetic* s, pgl_graph_view* view);
 int pgl_synthetic_free(pgl_synthetic* s);
 

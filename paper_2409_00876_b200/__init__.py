@@ -162,6 +162,8 @@ _sig = {
     "pgl_synthetic_generate": ([C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.POINTER(_vp)],
                                C.c_int),
     "pgl_synthetic_view": ([_vp, C.POINTER(_View)], C.c_int),
+    "pgl_synthetic_generate_nested": ([C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_double,
+                                       C.POINTER(_vp)], C.c_int),
     "pgl_synthetic_free": ([_vp], C.c_int),
     "pgl_layout_config_default": ([C.POINTER(_Cfg)], None),
     "pgl_layout_ext_default": ([C.POINTER(_Ext)], None),
@@ -478,6 +480,18 @@ def read_layout_tsv(path: str, threads: int = 0) -> np.ndarray:
         return np.ctypeslib.as_array(p, (4 * n.value,)).copy() if n.value else np.zeros(0)
     finally:
         _lib.pgl_free(p)
+
+
+def generate_nested_pangenome(seed: int, backbone_nodes: int, n_paths: int, depth: int = 3,
+                              site_rate: float = 0.05) -> PangenomeGraph:
+    """Config 5 fixture: nested bubbles, inversions, deletions, duplications
+    (pgl_synthetic_generate_nested)."""
+    h = C.c_void_p()
+    _check(_lib.pgl_synthetic_generate_nested(seed, backbone_nodes, n_paths, depth, site_rate, C.byref(h)))
+    owner = _SynthOwner(h)
+    v = _View()
+    _check(_lib.pgl_synthetic_view(h, C.byref(v)))
+    return PangenomeGraph._from_view(v, owner)
 
 
 def build_graph(node_lengths, walks, names=None) -> PangenomeGraph:

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -1002,6 +1003,120 @@ Synthetic* generate(uint64_t seed, uint64_t B, uint32_t n_paths, double rate) {
     return S.release();
 }
 
+// ---- config 5 fixture: nested bubbles, inversions, duplications ----------------
+// A deterministic high-complexity generator (not in the
+// reference, whose generator only makes SNV/indel bubbles). A backbone of B
+// nodes (lengths U[8, 32]) carries site records; each site spans [a, b) and
+// is one of
+//   substitution: an alternative branch of fresh nodes that is itself a
+//                 backbone with its own sites (nesting up to `depth` levels);
+//   inversion:    the span's nodes visited in reverse order and orientation;
+//   deletion:     the span skipped;
+//   duplication:  the span visited twice (node revisits within a path).
+// Every path walks the top backbone; at each site it takes the alternative
+// with the site's allele frequency (per path, per site draw). The result is
+// plain build_graph input (node lengths + oriented walks), so the reference
+// and the oracle can be handed the identical graph.
+struct NestedSite {
+    uint64_t a, b;        // span [a, b) on the level's backbone
+    uint8_t kind;         // 0 sub, 1 inv, 2 del, 3 dup
+    double freq;
+    int32_t child = -1;   // substitution: index of the alternative level
+};
+struct NestedLevel {
+    std::vector<uint32_t> nodes;   // the level's backbone node ids
+    std::vector<int32_t> site_at;  // site starting at backbone position, -1 none
+    std::vector<NestedSite> sites;
+};
+
+Synthetic* generate_nested(uint64_t seed, uint64_t B, uint32_t n_paths, uint32_t depth, double rate) {
+    if (B < 2) raise(PGL_ERR_INVALID_PARAMETER, "backbone needs at least 2 nodes");
+    if (n_paths < 1) raise(PGL_ERR_INVALID_PARAMETER, "need at least one path");
+    if (!(rate >= 0.0 && rate <= 0.5)) raise(PGL_ERR_INVALID_PARAMETER, "site rate must lie in [0, 0.5]");
+    auto S = std::make_unique<Synthetic>();
+    HostRng r(seed, kStreamSynth + 5);
+    std::vector<NestedLevel> levels;
+    auto new_node = [&]() {
+        S->node_len.push_back(8 + r.below(25));
+        return static_cast<uint32_t>(S->node_len.size() - 1);
+    };
+    // build a level of length L at nesting depth d; returns its index
+    std::function<int32_t(uint64_t, uint32_t)> build = [&](uint64_t L, uint32_t d) -> int32_t {
+        const int32_t id = static_cast<int32_t>(levels.size());
+        levels.emplace_back();
+        std::vector<uint32_t> nodes(L);
+        for (auto& n : nodes) n = new_node();
+        std::vector<int32_t> site_at(L, -1);
+        std::vector<NestedSite> sites;
+        for (uint64_t x = 0; x + 1 < L;) {
+            if (r.uniform() >= rate) {
+                ++x;
+                continue;
+            }
+            const uint64_t span = 1 + r.below(std::min<uint64_t>(L - x, d == 0 ? 64 : 16));
+            NestedSite st;
+            st.a = x;
+            st.b = x + span;
+            const uint64_t k = r.below(d + 1 < depth ? 4 : 3);  // deepest level: no substitutions
+            st.kind = static_cast<uint8_t>(k == 3 ? 0 : k + 1);
+            st.freq = 0.05 + 0.9 * r.uniform();
+            site_at[x] = static_cast<int32_t>(sites.size());
+            sites.push_back(st);
+            x = st.b;
+        }
+        for (auto& st : sites)
+            if (st.kind == 0) st.child = build(std::max<uint64_t>(1, (st.b - st.a) + r.below(8)), d + 1);
+        levels[id].nodes = std::move(nodes);
+        levels[id].site_at = std::move(site_at);
+        levels[id].sites = std::move(sites);
+        return id;
+    };
+    build(B, 0);
+    if (S->node_len.size() >= (1ULL << 32)) raise(PGL_ERR_INVALID_PARAMETER, "too many nodes");
+    S->paths.resize(n_paths);
+    for (uint32_t p = 0; p < n_paths; ++p) {
+        auto& steps = S->paths[p];
+        steps.reserve(B + B / 8);
+        uint64_t off = 0;
+        HostRng pr(seed ^ 0x5EED5EEDULL, kStreamSynth + 6 + p);
+        auto push = [&](uint32_t id, uint8_t rev) {
+            const uint32_t len = static_cast<uint32_t>(S->node_len[id]);
+            steps.push_back(pgl_path_step{off, id, len, rev, {}});
+            off += len;
+        };
+        std::function<void(int32_t)> walk = [&](int32_t lv) {
+            const NestedLevel& L = levels[lv];
+            uint64_t x = 0;
+            while (x < L.nodes.size()) {
+                const int32_t si = L.site_at[x];
+                if (si >= 0 && pr.uniform() < L.sites[si].freq) {
+                    const NestedSite& st = L.sites[si];
+                    switch (st.kind) {
+                        case 0: walk(st.child); break;
+                        case 1:
+                            for (uint64_t y = st.b; y-- > st.a;) push(L.nodes[y], 1);
+                            break;
+                        case 2: break;
+                        default:
+                            for (int rep = 0; rep < 2; ++rep)
+                                for (uint64_t y = st.a; y < st.b; ++y) push(L.nodes[y], 0);
+                    }
+                    x = st.b;
+                    continue;
+                }
+                push(L.nodes[x], 0);
+                ++x;
+            }
+        };
+        walk(0);
+        if (steps.empty()) push(levels[0].nodes[0], 0);
+        S->totals.push_back(off);
+        S->n_steps.push_back(steps.size());
+        S->ptrs.push_back(steps.data());
+    }
+    return S.release();
+}
+
 }  // namespace
 
 struct pgl_synthetic : Synthetic {};
@@ -1296,6 +1411,15 @@ int pgl_synthetic_generate(uint64_t seed, uint64_t backbone, uint32_t n_paths, d
     return guarded([&] {
         if (!out) raise(PGL_ERR_INVALID_PARAMETER, "out is null");
         *out = static_cast<pgl_synthetic*>(generate(seed, backbone, n_paths, rate));
+    });
+}
+
+int pgl_synthetic_generate_nested(uint64_t seed, uint64_t backbone, uint32_t n_paths, uint32_t depth,
+                                  double site_rate, pgl_synthetic** out) {
+    return guarded([&] {
+        if (!out) raise(PGL_ERR_INVALID_PARAMETER, "out is null");
+        if (depth < 1 || depth > 8) raise(PGL_ERR_INVALID_PARAMETER, "nesting depth must lie in [1, 8]");
+        *out = static_cast<pgl_synthetic*>(generate_nested(seed, backbone, n_paths, depth, site_rate));
     });
 }
 

@@ -376,3 +376,53 @@ def test_sps_stream_revisits(pgl, oracle, ref, gpu):
     want = ref.sps(gr, lay, 17, 200)
     assert (got.n, got.skipped) == (want.n, want.skipped)
     assert got.mean == pytest.approx(want.mean, rel=1e-12)
+
+
+# ---- config 5: nested bubbles, inversions, duplications ------------------------------
+
+C5_SMALL = (5, 3000, 50, 3, 0.05)  # generate_nested_pangenome args (the full config: backbone 2e5, 500 paths)
+
+
+def nested_pair(pgl, ref, args):
+    g = pgl.generate_nested_pangenome(*args)
+    walks = [list(zip(s["node_id"].tolist(), s["orient"].tolist())) for s in g.path_steps]
+    return g, ref.build(g.node_len.tolist(), walks)
+
+
+def test_nested_graph_index_matches_reference(pgl, ref, gpu):
+    """The fixture is plain build_graph input: the reference builds the same
+    index (positions of reverse steps and revisits included)."""
+    g, gr = nested_pair(pgl, ref, C5_SMALL)
+    with pgl.DeviceGraph(g) as dg:
+        pos, nodes, cum = dg.export_index()
+    fo = ref.export(gr)
+    assert np.array_equal(cum, fo.cum) and np.array_equal(nodes, fo.step_node)
+    assert np.array_equal(pos, fo.positions())
+
+
+@pytest.mark.slow
+def test_hogwild_sps_parity_config5(pgl, ref, gpu):
+    """North-star gate on the high-complexity shape (long Zipf jumps:
+    zipf_space_max 1e5): median SPS over seeds 101..105 within 2% of the
+    reference's threads=1 layouts, same estimator and metric seed."""
+    g, gr = nested_pair(pgl, ref, C5_SMALL)
+    gpu_sps, cpu_sps = [], []
+    for seed in range(101, 106):
+        cfg = dict(global_seed=seed, zipf_space_max=100000)
+        out = pgl.run_layout(g, pgl.LayoutConfig(**cfg))
+        gpu_sps.append(ref.sps(gr, out, 7, 20).mean)
+        lay, _ = ref.run_layout(gr, make_cfg(**cfg))
+        cpu_sps.append(ref.sps(gr, lay, 7, 20).mean)
+    ratio = np.median(gpu_sps) / np.median(cpu_sps)
+    assert 0.98 <= ratio <= 1.02, (gpu_sps, cpu_sps, ratio)
+
+
+def test_replay_bit_exact_nested(pgl, oracle, ref, gpu):
+    """Replay mode on inversions + revisits: bit-exact with the reference."""
+    g, gr = nested_pair(pgl, ref, (9, 300, 6, 3, 0.1))
+    cfg = dict(n_iters=4, global_seed=3, zipf_space_max=100000)
+    st = pgl.RunStats()
+    out = pgl.run_layout(g, pgl.LayoutConfig(**cfg), stats=st, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    lay, rst = ref.run_layout(gr, make_cfg(**cfg))
+    assert stats_tuple(st) == stats_tuple(rst)
+    np.testing.assert_allclose(out, lay, rtol=1e-9, atol=1e-9)  # jitter path: cos/sin within 1e-9
