@@ -225,8 +225,7 @@ def cpu_reference_sample(args, n_steps_total=1, budget_s=20.0):
     if args.config == "c5":  # the fixture's walks, built by the reference's own build_graph
         import paper_2409_00876_b200 as P
         gp = make_graph(P, "c5")
-        g = R.build(gp.node_len.tolist(),
-                    [list(zip(s["node_id"].tolist(), s["orient"].tolist())) for s in gp.path_steps])
+        g = R.build_steps(gp.node_len, gp.path_steps)
         del gp
     else:
         g = R.generate(*CONFIGS[args.config], gfa_roundtrip=(args.config == "c1"))

@@ -352,6 +352,17 @@ class Reference:
                                           ptr(sn, u32p), ptr(sr, u8p), C.byref(h)))
         return self._wrap(h)
 
+    def build_steps(self, node_len, path_steps):
+        """build_graph from PathStep-dtype arrays (node_id, orient per path), numpy only."""
+        nl = np.asarray(node_len, np.uint64)
+        pn = np.asarray([len(p) for p in path_steps], np.uint64)
+        sn = np.ascontiguousarray(np.concatenate([p["node_id"] for p in path_steps]), np.uint32)
+        sr = np.ascontiguousarray(np.concatenate([p["orient"] for p in path_steps]), np.uint8)
+        h = C.c_void_p()
+        self._check(self.lib.pglref_build(len(nl), ptr(nl, u64p), len(path_steps), ptr(pn, u64p),
+                                          ptr(sn, u32p), ptr(sr, u8p), C.byref(h)))
+        return self._wrap(h)
+
     def export(self, g) -> FlatGraph:
         c = np.array([g.n_nodes, g.n_paths, g.total_steps], np.uint64)
         return _export(self.lib, "pglref_", g.h, c)

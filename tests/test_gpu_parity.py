@@ -385,8 +385,7 @@ C5_SMALL = (5, 3000, 50, 3, 0.05)  # generate_nested_pangenome args (the full co
 
 def nested_pair(pgl, ref, args):
     g = pgl.generate_nested_pangenome(*args)
-    walks = [list(zip(s["node_id"].tolist(), s["orient"].tolist())) for s in g.path_steps]
-    return g, ref.build(g.node_len.tolist(), walks)
+    return g, ref.build_steps(g.node_len, g.path_steps)
 
 
 def test_nested_graph_index_matches_reference(pgl, ref, gpu):
