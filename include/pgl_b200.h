@@ -126,19 +126,13 @@ typedef enum pgl_sampling {
     PGL_SAMPLING_IID = 1
 } pgl_sampling;
 
-/* Order in which the tile sampler visits its units of 32 picks. Either way
- * every unit is visited exactly once per iteration; only which units run
- * concurrently changes. */
+/* Order in which the tile sampler visits its units of 32 picks. */
 typedef enum pgl_unit_order {
-    PGL_ORDER_AUTO = 0,   /* = PGL_ORDER_SPREAD (measured: fronts gain nothing once
-                             uniform partners share a window) */
-    /* u = (a*k + b) mod U, a ~ U/phi: concurrent warps spread over the whole
-     * graph (every partner gather is a cold random line). */
+    PGL_ORDER_AUTO = 0,   /* = PGL_ORDER_SPREAD */
+    /* u = (a*k + b) mod U, a ~ U/phi: concurrent warps spread over the whole graph */
     PGL_ORDER_SPREAD = 1,
-    /* The unit space is cut into F contiguous stretches ("fronts", F prime,
-     * ~front_warps concurrent warps each) swept in parallel, alternating
-     * direction per iteration, rotated by a fresh offset, so Zipf partners
-     * fall in the recent trail of their own front. */
+    /* contiguous sweep fronts: measured no faster once partners are windowed;
+     * rejected (InvalidParameter) by this build, the value stays reserved */
     PGL_ORDER_FRONTS = 2
 } pgl_unit_order;
 
@@ -157,15 +151,14 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t kernel_variant;  /* tile kernel: 0 = auto; 1 = two-stage pipeline, 2 CTAs/SM;
-                                 2 = two-stage, 3 CTAs/SM; 3 = three-stage (early endpoint
-                                 loads), 3 CTAs/SM; 4 = four-stage with L2 prefetch;
-                                 5/6 = cp.async pipeline via shared memory, 4/3 CTAs/SM.
+    uint32_t kernel_variant;  /* tile kernel: 0 = auto; 1 = register pipeline, 2 CTAs/SM;
+                                 2 = register pipeline, 3 CTAs/SM; 5/6 = cp.async pipeline
+                                 via shared memory, 4/3 CTAs/SM.
                                  i.i.d. kernel: 0 = 2 CTAs/SM, 1 = 3 CTAs/SM */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
     uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */
     uint32_t unit_order;      /* pgl_unit_order (tile sampling only) */
-    uint32_t front_warps;     /* warps per sweep front (PGL_ORDER_FRONTS); 0 = auto */
+    uint32_t front_warps;     /* reserved (was: warps per sweep front) */
     uint32_t pair_window;     /* 0 = auto (= 3), 1 = independent partner draws,
                                  2 = one shared random window per unit (see pgl_tiles.cu),
                                  3 = 2 + one shared Zipf hop per unit in cooling batches */

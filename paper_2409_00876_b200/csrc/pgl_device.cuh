@@ -252,14 +252,6 @@ __device__ __forceinline__ uint64_t zipf_alias(const ZipfAlias* tab, uint32_t zn
     return 1 + (static_cast<uint32_t>(x) < e.x ? col : e.y);
 }
 
-// L2 prefetches for the pipelined tile kernel: a bulk (TMA-engine) prefetch of
-// a contiguous byte range, and a one-sector prefetch of a coordinate endpoint.
-__device__ __forceinline__ void prefetch_bulk_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void prefetch_l2_keep(const void* p) {
-    asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(p));
-}
 // Asynchronous global -> shared copies (LDGSTS), completion tracked per
 // thread by commit/wait groups: the loads hold no registers while in flight.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -565,27 +565,12 @@ pgl_graph_view view_of(const pgl_graph* G) {
     return v;
 }
 
-constexpr uint32_t kFrontWarps = 8;  // default concurrent warps per sweep front
-constexpr uint32_t kHopLanes = 8;    // default lanes per shared Zipf hop
-
-uint64_t next_prime(uint64_t n) {
-    if (n <= 2) return 2;
-    for (uint64_t c = n | 1;; c += 2) {
-        bool prime = true;
-        for (uint64_t d = 3; d * d <= c; d += 2)
-            if (c % d == 0) {
-                prime = false;
-                break;
-            }
-        if (prime) return c;
-    }
-}
+constexpr uint32_t kHopLanes = 8;  // default lanes per shared Zipf hop
 
 // Tile-kernel variant (pgl_tiles.cu): auto = the asynchronous cp.async
 // pipeline at 3 CTAs/SM once the concurrency cap no longer binds (the graph
-// fills the GPU), else the two-stage kernel, whose shorter read-to-write
-// window keeps small graphs' layouts closest to the reference. The fronts
-// order runs on the two-stage kernel only.
+// fills the GPU), else the register pipeline, whose shorter read-to-write
+// window keeps small graphs' layouts closest to the reference.
 int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
     int v = static_cast<int>(ext.kernel_variant & 15);
     const int force64 = static_cast<int>(ext.kernel_variant & 16);
@@ -594,7 +579,8 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
         PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         v = cap >= static_cast<uint32_t>(sms) * 3 * 8 ? 6 : 1;
     }
-    if (ext.unit_order == PGL_ORDER_FRONTS && v > 2) v = 1;
+    if (v != 1 && v != 2 && v != 5 && v != 6)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5, 6");
     return v | force64;
 }
 
@@ -623,6 +609,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.struct_size mismatch");
         std::memcpy(&ext, extp, extp->struct_size);
     }
+    if (ext.unit_order == PGL_ORDER_FRONTS)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the fronts order is not available in this build");
     if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.hop_lanes must be 0 or a power of two <= 32");
     if (reuse) {  // run_layout_reuse, engine.cpp:328-334
@@ -787,19 +775,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
                 const uint64_t uw = static_cast<uint64_t>((static_cast<unsigned __int128>(U) * 32) % S);
                 a.i0_wrap = (a.i0_step + S - uw) % S;
             }
-            a.fronts = a.front_len = a.front_rem = 0;
-            a.reverse = it & 1;
             a.pair_window = ext.pair_window == 1 ? 0 : (ext.pair_window == 2 ? 1 : 3);
             a.record_hint = ext.record_hint;
             a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : kHopLanes;
-            if (ext.unit_order == PGL_ORDER_FRONTS) {
-                // F prime (so fronts of different passes never sit on the same
-                // step: F does not divide 10/srf) near n_warps / front_warps
-                const uint64_t want = std::max<uint64_t>(1, n_warps / (ext.front_warps ? ext.front_warps : kFrontWarps));
-                a.fronts = std::min<uint64_t>(next_prime(want), U);
-                a.front_len = U / a.fronts;
-                a.front_rem = U % a.fronts;
-            }
         }
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
         if (replay)

@@ -88,16 +88,10 @@ struct IterArgs {
     uint64_t perm_step;   // (a * n_warps) mod U
     uint64_t i0_step;     // (32 * perm_step) mod S: first-step advance of a round
     uint64_t i0_wrap;     // (32 * (perm_step - U)) mod S: the same when u wraps
-    // fronts order (fronts > 0): k -> front f = k mod F, t = k div F;
-    // u = (start_f + (reverse ? len_f - 1 - t : t) + perm_b) mod U with
-    // len_f = front_len + (f < front_rem), start_f = f*front_len + min(f, front_rem)
-    uint64_t fronts;      // F (0 = spread order)
-    uint64_t front_len;   // U div F
-    uint64_t front_rem;   // U mod F
-    uint32_t reverse;     // sweep direction of this iteration
-    uint32_t pair_window; // uniform partners from one shared random window per unit
+    uint32_t pair_window; // 0 independent partners, 1 shared uniform window, 3 window + shared Zipf hop
     uint32_t record_hint; // 0 = records evict_first in L2, 1 = evict_normal
     uint32_t hop_lanes;   // lanes sharing one Zipf hop (pair_window 3): 1..32, power of two
+    uint32_t _pad0;
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].

@@ -59,15 +59,14 @@ struct TileSel {
     uint32_t flags;       // bit0 valid, bit1 e_i end, bit2 e_j end, bit3 j in tile
 };
 
-// kDepth 2 (default): select(m+1) overlapped with update(m). kDepth 4
-// (variant 2, spread order only): a four-stage software pipeline per warp,
-// one unit per stage, so every load is issued one round before it is used:
-//   A  unit m+3: bulk L2 prefetch of its 512 record bytes (TMA engine, lane 0)
-//   B  unit m+2: batch coin, path, partner selection; record loads (L2 hits)
-//   C  unit m+1: in-tile partner records by shuffle; L2 prefetch of the two
-//                coordinate endpoints
-//   D  unit m:   endpoint loads (L2 hits), update, write-back
-template <typename T, int kMinBlocks, int kDepth, bool k32>
+// Two pipelines per warp, one unit of 32 picks per round:
+//   register (kAsync = false): select(m+1) -- batch coin, path, partner,
+//     record loads into registers -- overlapped with update(m) (endpoint
+//     loads, arithmetic, write-back);
+//   asynchronous (kAsync = true): records and endpoints are copied global ->
+//     shared with cp.async (no registers held while in flight), three units in
+//     flight: endpoints of m landing, records of m+1 landing, m+2 selected.
+template <typename T, int kMinBlocks, bool kAsync, bool k32>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                 DevStats* stats, IterArgs a) {
     // k32: every step index, unit index and path length fits in 31 bits
@@ -86,42 +85,15 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     const UX U = static_cast<UX>(a.units);
     const UX n_mine = warp < U ? static_cast<UX>((U - warp + a.n_warps - 1) / a.n_warps) : 0;  // k = w + m*W < U
     UX u = warp < U ? static_cast<UX>((a.perm_a * static_cast<uint64_t>(warp) + a.perm_b) % a.units) : 0;
-    uint64_t k = warp;  // this warp's visit index, k = w + m*W
-    // fronts order: unit of visit index k (see IterArgs)
-    auto front_unit = [&](uint64_t kk) -> uint64_t {
-        const uint64_t f = kk % a.fronts, t = kk / a.fronts;
-        const uint64_t len = a.front_len + (f < a.front_rem ? 1 : 0);
-        const uint64_t start = f * a.front_len + (f < a.front_rem ? f : a.front_rem);
-        const uint64_t uu = start + (a.reverse ? len - 1 - t : t) + a.perm_b;
-        return uu >= U ? uu - U : uu;
-    };
-    if (a.fronts && warp < U) u = static_cast<UX>(front_unit(k));
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
     bool carry = false;
     uint32_t b0 = 0;  // this warp's step count mod batch (batch boundaries, engine.cpp:115-124)
 
     // Stage A: batch decision, i's record (coalesced), partner selection.
-    // path of the lane's step in a unit (sguide + cum, L1-resident)
-    struct Loc {
-        uint32_t p;
-        UX pbase;
-        SX n;
-    };
-    auto locate = [&](UX unit, UX unit_i0) -> Loc {
-        Loc l{0, 0, 0};
-        if (static_cast<uint64_t>(unit) * 32 + lane < a.steps) {
-            UX gi = unit_i0 + lane;
-            while (gi >= S) gi -= S;
-            l.p = path_of_step(g, gi);
-            l.pbase = static_cast<UX>(__ldg(g.cum + l.p));
-            l.n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + l.p + 1)) - l.pbase);
-        }
-        return l;
-    };
-    StepRec* async_ri = nullptr;  // kDepth 5: shared-memory destinations of select's record copies
+    StepRec* async_ri = nullptr;  // kAsync: shared-memory destinations of select's record copies
     StepRec* async_rj = nullptr;
-    auto select = [&](UX unit, UX unit_i0, const Loc* pre) -> TileSel {
+    auto select = [&](UX unit, UX unit_i0) -> TileSel {
         TileSel o;
         o.flags = 0;
         o.src = 0;
@@ -166,11 +138,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         uint32_t p = 0;
         UX pbase = 0;
         SX n = 0;
-        if (pre) {
-            p = pre->p;
-            pbase = pre->pbase;
-            n = pre->n;
-        } else if (active) {
+        if (active) {
             p = path_of_step(g, gi);
             pbase = static_cast<UX>(__ldg(g.cum + p));
             n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + p + 1)) - pbase);
@@ -203,7 +171,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const bool shared = ((tag >> 30) & 1) && ((tag >> 29) & 1) == (cooling ? 1u : 0u) && (tag & 0x1FFFFFFFu) == p;
         // the unit's records (one coalesced 512-byte load), issued after the
         // path lookup so its DRAM latency is waited for only in next round's update
-        if constexpr (kDepth == 5)
+        if constexpr (kAsync)
             cp_async<16>(async_ri + lane, g.step + gi, pol_stream);
         else
             o.ri = load_step_stream(g.step + gi, pol_stream);
@@ -247,7 +215,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             fl |= 8u;
             o.src = static_cast<uint32_t>(gj - i0);
         } else {
-            if constexpr (kDepth == 5)
+            if constexpr (kAsync)
                 cp_async<16>(async_rj + lane, g.step + gj, pol_stream);
             else
                 o.rj = load_step_stream(g.step + gj, pol_stream);
@@ -300,28 +268,22 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
         if (ii >= S) ii -= S;
     };
-    if (kDepth == 2) {
+    if constexpr (!kAsync) {
         if (n_mine) {
-            TileSel cur = select(u, i0, nullptr);
+            TileSel cur = select(u, i0);
             for (UX m = 0; m < n_mine; ++m) {
                 TileSel nxt;
                 nxt.flags = 0;
                 nxt.src = 0;
                 if (m + 1 < n_mine) {
-                    k += a.n_warps;
-                    if (a.fronts) {
-                        u = static_cast<UX>(front_unit(k));
-                        i0 = static_cast<UX>((static_cast<uint64_t>(u) * 32) % g.total_steps);
-                    } else {
-                        advance(u, i0);
-                    }
-                    nxt = select(u, i0, nullptr);
+                    advance(u, i0);
+                    nxt = select(u, i0);
                 }
                 applied += update(cur);
                 cur = nxt;
             }
         }
-    } else if (kDepth == 5) {
+    } else {
         // Asynchronous pipeline: records and endpoints travel global ->
         // shared by cp.async (no registers held while in flight). Round m:
         //   1. wait for the endpoints of unit m, apply its update;
@@ -342,7 +304,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         auto issue_sel = [&](UX m, UX uu, UX ii) -> uint32_t {
             async_ri = s_ri[m % 3][wib];
             async_rj = s_rj[m % 3][wib];
-            const TileSel t = select(uu, ii, nullptr);
+            const TileSel t = select(uu, ii);
             cp_async_commit();
             return t.flags | (t.src << 8);
         };
@@ -418,148 +380,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 cur = nres;
             }
         }
-    } else if (kDepth == 3) {
-        // two-stage, with the endpoint loads of unit m issued before the
-        // selection work of unit m+1 so the latter hides their latency
-        if (n_mine) {
-            TileSel cur = select(u, i0, nullptr);
-            for (UX m = 0; m < n_mine; ++m) {
-                // the next unit's path lookup first: its (L1) loads must not
-                // share a scoreboard with the endpoint gathers issued below
-                Loc nloc{0, 0, 0};
-                UX nu = u, ni0 = i0;
-                if (m + 1 < n_mine) {
-                    advance(nu, ni0);
-                    nloc = locate(nu, ni0);
-                }
-                StepRec sh;
-                sh.node = __shfl_sync(kFull, cur.ri.node, cur.src);
-                sh.ps_lo = __shfl_sync(kFull, cur.ri.ps_lo, cur.src);
-                sh.pe_lo = __shfl_sync(kFull, cur.ri.pe_lo, cur.src);
-                sh.hi = __shfl_sync(kFull, cur.ri.hi, cur.src);
-                if (cur.flags & 8u) cur.rj = sh;
-                const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
-                double d_ref = 0.0, vix = 0, viy = 0, vjx = 0, vjy = 0;
-                if (cur.flags & 1u) {
-                    d_ref = abs_diff(step_pos(cur.ri, ei), step_pos(cur.rj, ej));
-                    if (d_ref > 0.0) {
-                        CoordHint<T>::get(coords, cur.ri.node, ei, pol_keep, vix, viy);
-                        CoordHint<T>::get(coords, cur.rj.node, ej, pol_keep, vjx, vjy);
-                    }
-                }
-                TileSel nxt;
-                nxt.flags = 0;
-                nxt.src = 0;
-                if (m + 1 < n_mine) {
-                    u = nu;
-                    i0 = ni0;
-                    nxt = select(u, i0, &nloc);
-                }
-                if ((cur.flags & 1u) && d_ref > 0.0)
-                    applied += hog_apply_t<T>(coords, cur.ri.node, ei, cur.rj.node, ej, d_ref, a.eta, r, pol_keep,
-                                              vix, viy, vjx, vjy);
-                if ((cur.flags & 1u) && a.drf > 1) {
-                    unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
-                    for (uint32_t extra = 1; extra < a.drf; ++extra) {
-                        int ea, eb;
-                        do {
-                            const uint64_t b2 = r.next();
-                            ea = (b2 >> 63) ? 0 : 1;
-                            eb = ((b2 >> 62) & 1) ? 0 : 1;
-                        } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
-                        used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                        applied += hog_update_t<T>(coords, cur.ri.node, ea, cur.rj.node, eb,
-                                                   abs_diff(step_pos(cur.ri, ea), step_pos(cur.rj, eb)), a.eta, r,
-                                                   pol_keep);
-                    }
-                }
-                cur = nxt;
-            }
-        }
-    } else if (n_mine) {
-        // Stage A: the unit's record bytes into L2 (wrapping at the end of a pass)
-        auto prefetch_unit = [&](UX uu, UX ii) {
-            if (S < 32) return;  // warp-uniform arguments: one UBLKPF per warp
-            const uint64_t q0 = static_cast<uint64_t>(uu) * 32;
-            const uint32_t n_act = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
-            const uint32_t first = static_cast<uint32_t>(S - ii < n_act ? S - ii : n_act);
-            prefetch_bulk_l2(g.step + ii, first * static_cast<uint32_t>(sizeof(StepRec)));
-            if (first < n_act) prefetch_bulk_l2(g.step, (n_act - first) * static_cast<uint32_t>(sizeof(StepRec)));
-        };
-        // Stage C: resolve in-tile partners, prefetch both endpoints into L2
-        auto resolve = [&](TileSel& o) {
-            StepRec sh;
-            sh.node = __shfl_sync(kFull, o.ri.node, o.src);
-            sh.ps_lo = __shfl_sync(kFull, o.ri.ps_lo, o.src);
-            sh.pe_lo = __shfl_sync(kFull, o.ri.pe_lo, o.src);
-            sh.hi = __shfl_sync(kFull, o.ri.hi, o.src);
-            if (o.flags & 8u) o.rj = sh;
-            if (o.flags & 1u) {
-                prefetch_l2_keep(coord_addr<T>(coords, o.ri.node, (o.flags >> 1) & 1));
-                prefetch_l2_keep(coord_addr<T>(coords, o.rj.node, (o.flags >> 2) & 1));
-            }
-        };
-        UX pu = u, pi = i0;  // prefetch cursor: one unit ahead of the select cursor
-        prefetch_unit(pu, pi);
-        for (int t = 1; t < 3 && t < static_cast<int>(n_mine); ++t) {
-            advance(pu, pi);
-            prefetch_unit(pu, pi);
-        }
-        TileSel cur = select(u, i0, nullptr);  // unit 0
-        resolve(cur);
-        TileSel nxt;
-        nxt.flags = 0;
-        nxt.src = 0;
-        if (n_mine > 1) {
-            advance(u, i0);
-            nxt = select(u, i0, nullptr);      // unit 1
-        }
-        for (UX m = 0; m < n_mine; ++m) {
-            if (m + 3 < n_mine) {
-                advance(pu, pi);
-                prefetch_unit(pu, pi);
-            }
-            // Stage D loads for unit m
-            const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
-            double d_ref = 0.0;
-            double vix = 0, viy = 0, vjx = 0, vjy = 0;
-            if (cur.flags & 1u) {
-                d_ref = abs_diff(step_pos(cur.ri, ei), step_pos(cur.rj, ej));
-                if (d_ref > 0.0) {
-                    CoordHint<T>::get(coords, cur.ri.node, ei, pol_keep, vix, viy);
-                    CoordHint<T>::get(coords, cur.rj.node, ej, pol_keep, vjx, vjy);
-                }
-            }
-            TileSel nn;
-            nn.flags = 0;
-            nn.src = 0;
-            if (m + 2 < n_mine) {
-                advance(u, i0);
-                nn = select(u, i0, nullptr);   // stage B, unit m+2
-            }
-            if (m + 1 < n_mine) resolve(nxt);  // stage C, unit m+1
-            // Stage D arithmetic + write-back for unit m
-            if ((cur.flags & 1u) && d_ref > 0.0)
-                applied += hog_apply_t<T>(coords, cur.ri.node, ei, cur.rj.node, ej, d_ref, a.eta, r, pol_keep,
-                                          vix, viy, vjx, vjy);
-            if ((cur.flags & 1u) && a.drf > 1) {
-                unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
-                for (uint32_t extra = 1; extra < a.drf; ++extra) {
-                    int ea, eb;
-                    do {
-                        const uint64_t b2 = r.next();
-                        ea = (b2 >> 63) ? 0 : 1;
-                        eb = ((b2 >> 62) & 1) ? 0 : 1;
-                    } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
-                    used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                    applied += hog_update_t<T>(coords, cur.ri.node, ea, cur.rj.node, eb,
-                                               abs_diff(step_pos(cur.ri, ea), step_pos(cur.rj, eb)), a.eta, r,
-                                               pol_keep);
-                }
-            }
-            cur = nxt;
-            nxt = nn;
-        }
     }
 
     rng.s0[tid] = r.a;
@@ -575,25 +395,21 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 
 // Tile-kernel variants (pgl_layout_ext.kernel_variant; 0 = auto, chosen by
 // the host):
-//   1  two-stage pipeline, 2 CTAs/SM (no spills); auto where the concurrency
+//   1  register pipeline, 2 CTAs/SM (no spills); auto where the concurrency
 //      cap binds (small graphs: the shortest read-to-write window)
-//   2  two-stage pipeline, 3 CTAs/SM (80 registers)
-//   3  three-stage: endpoint loads of unit m issued before the selection of
-//      unit m+1, 3 CTAs/SM
-//   4  four-stage pipeline with bulk L2 prefetch of records and endpoints
-//   5  asynchronous pipeline (cp.async records and endpoints staged in shared
-//      memory), 4 CTAs/SM (64 registers)
-//   6  the same at 3 CTAs/SM; auto once the graph fills the GPU (configs 2-5:
-//      C2 43 G upd/s vs 39-41 for variants 1/3)
-// Bit 4 forces the 64-bit index instantiation (measurements).
+//   2  register pipeline, 3 CTAs/SM (80 registers)
+//   5  asynchronous pipeline, 4 CTAs/SM (64 registers)
+//   6  asynchronous pipeline, 3 CTAs/SM; auto once the graph fills the GPU
+//      (config 2: 43 G upd/s vs 39 for variant 1)
+// (3 and 4 were a three-stage register pipeline and a bulk-L2-prefetch
+// four-stage pipeline; measured no better, removed.) Bit 4 forces the
+// 64-bit index instantiation (measurements).
 template <typename T, bool k32>
 const void* tiles_fn_t(int variant) {
-    return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 2, k32>)
-           : variant == 3 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 3, k32>)
-           : variant == 4 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 4, k32>)
-           : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 5, k32>)
-           : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 5, k32>)
-                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 2, k32>);
+    return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, false, k32>)
+           : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, true, k32>)
+           : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, true, k32>)
+                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, false, k32>);
 }
 
 template <typename T>

@@ -1,6 +1,6 @@
 """Short target for ncu: one layout of a config with few iterations.
 usage: python tools/prof_target.py CONFIG ITERS PREC [ORDER [FRONT_WARPS]]
-ORDER: 0 auto, 1 spread, 2 fronts (pgl_unit_order)."""
+ORDER: pgl_unit_order (0 auto = 1 spread)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
