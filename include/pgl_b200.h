@@ -164,7 +164,11 @@ typedef struct pgl_layout_ext {
                                  3 = 2 + one shared Zipf hop per unit in cooling batches */
     uint32_t record_hint;     /* L2 policy of step-record loads: 0 = evict_first, 1 = evict_normal */
     uint32_t hop_lanes;       /* lanes sharing one Zipf hop (pair_window 3); 0 = auto (8) */
-    uint32_t _reserved[2];
+    uint32_t reuse_shuffle;   /* drf > 1: 0 = the reference's re-update of the same step pair
+                                 under unused endpoint combinations (engine.cpp:147-170);
+                                 1 = warp-level data reuse (paper §7.4): extra updates pair
+                                 this lane's i with another lane's partner, from registers */
+    uint32_t _reserved[1];
 } pgl_layout_ext;
 
 void pgl_layout_ext_default(pgl_layout_ext* ext);

@@ -73,7 +73,7 @@ class _Ext(C.Structure):
                 ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
                 ("sampling", C.c_uint32), ("unit_order", C.c_uint32), ("front_warps", C.c_uint32),
                 ("pair_window", C.c_uint32), ("record_hint", C.c_uint32), ("hop_lanes", C.c_uint32),
-                ("_reserved", C.c_uint32 * 2)]
+                ("reuse_shuffle", C.c_uint32), ("_reserved", C.c_uint32 * 1)]
 
 
 class _PathStep(C.Structure):
@@ -262,6 +262,7 @@ class LayoutExt:
     pair_window: int = 0  # 0 auto (= 3), 1 independent draws, 2 shared uniform window, 3 window + shared Zipf hop
     record_hint: int = 0  # 0 evict_first, 1 evict_normal
     hop_lanes: int = 0  # lanes per shared Zipf hop (pair_window 3), 0 = auto
+    reuse_shuffle: int = 0  # drf > 1 extras by warp-shuffle reuse (paper §7.4)
 
     def _c(self) -> _Ext:
         e = _Ext()
@@ -273,6 +274,7 @@ class LayoutExt:
         e.sampling = self.sampling
         e.unit_order, e.front_warps = self.unit_order, self.front_warps
         e.pair_window, e.record_hint, e.hop_lanes = self.pair_window, self.record_hint, self.hop_lanes
+        e.reuse_shuffle = self.reuse_shuffle
         return e
 
 

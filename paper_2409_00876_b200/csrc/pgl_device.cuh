@@ -292,12 +292,26 @@ __device__ __forceinline__ uint32_t hog_update_t(void* coords, uint32_t ni, int 
     return hog_apply_t<T>(coords, ni, ei, nj, ej, d_ref, eta, r, pol, vix, viy, vjx, vjy);
 }
 
+// hog_apply_t that also returns the new v_i (warp-shuffle reuse keeps
+// updating the same i endpoint).
+template <typename T>
+__device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                                 double d_ref, double eta, Xo& r, uint64_t pol, double& vix,
+                                                 double& viy, double vjx, double vjy);
+
 // The arithmetic and write-back half of hog_update_t, on endpoint values the
 // caller loaded (d_ref > 0).
 template <typename T>
 __device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
                                               double d_ref, double eta, Xo& r, uint64_t pol, double vix,
                                               double viy, double vjx, double vjy) {
+    return hog_apply_io_t<T>(coords, ni, ei, nj, ej, d_ref, eta, r, pol, vix, viy, vjx, vjy);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
+                                                 double d_ref, double eta, Xo& r, uint64_t pol, double& vix,
+                                                 double& viy, double vjx, double vjy) {
     double mu = eta * rcp_nr(d_ref * d_ref);
     if (mu > 1.0) mu = 1.0;
     const double dx = vix - vjx;
@@ -317,7 +331,9 @@ __device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int e
         uy = dy * rs;
     }
     const double delta = mu * (mag - d_ref) * 0.5;
-    CoordHint<T>::set(coords, ni, ei, pol, vix - delta * ux, viy - delta * uy);
+    vix -= delta * ux;
+    viy -= delta * uy;
+    CoordHint<T>::set(coords, ni, ei, pol, vix, viy);
     CoordHint<T>::set(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy);
     return 1;
 }

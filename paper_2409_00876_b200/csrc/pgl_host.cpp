@@ -609,6 +609,10 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.struct_size mismatch");
         std::memcpy(&ext, extp, extp->struct_size);
     }
+    if (ext.reuse_shuffle && (ext.mode != PGL_MODE_HOGWILD || ext.sampling != PGL_SAMPLING_TILES))
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle needs the Hogwild tile sampler");
+    if (ext.reuse_shuffle && G->n_paths >= (1u << 19))
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle supports fewer than 2^19 paths");
     if (ext.unit_order == PGL_ORDER_FRONTS)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the fronts order is not available in this build");
     if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
@@ -778,6 +782,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.pair_window = ext.pair_window == 1 ? 0 : (ext.pair_window == 2 ? 1 : 3);
             a.record_hint = ext.record_hint;
             a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : kHopLanes;
+            a.reuse_shuffle = ext.reuse_shuffle ? 1 : 0;
         }
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
         if (replay)

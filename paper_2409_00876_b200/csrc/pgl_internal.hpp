@@ -91,7 +91,7 @@ struct IterArgs {
     uint32_t pair_window; // 0 independent partners, 1 shared uniform window, 3 window + shared Zipf hop
     uint32_t record_hint; // 0 = records evict_first in L2, 1 = evict_normal
     uint32_t hop_lanes;   // lanes sharing one Zipf hop (pair_window 3): 1..32, power of two
-    uint32_t _pad0;
+    uint32_t reuse_shuffle;  // drf > 1 extras by warp-shuffle reuse (paper §7.4) instead of endpoint combos
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].

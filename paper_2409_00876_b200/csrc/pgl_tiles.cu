@@ -57,6 +57,7 @@ struct TileSel {
     StepRec ri, rj;       // rj valid when !(flags & 8)
     uint32_t src;         // lane holding j's record when in-tile
     uint32_t flags;       // bit0 valid, bit1 e_i end, bit2 e_j end, bit3 j in tile
+    uint32_t path;        // path of i (warp-shuffle reuse pairs only within a path)
 };
 
 // Two pipelines per warp, one unit of 32 picks per round:
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         TileSel o;
         o.flags = 0;
         o.src = 0;
+        o.path = 0;
         o.ri = o.rj = StepRec{0, 0, 0, 0};
         const uint64_t q0 = static_cast<uint64_t>(unit) * 32;
         const bool active = q0 + lane < a.steps;
@@ -221,7 +223,39 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 o.rj = load_step_stream(g.step + gj, pol_stream);
         }
         o.flags = fl;
+        o.path = p;
         return o;
+    };
+
+    // Warp-level data reuse (paper 2409.00876 §7.4, pgl_layout_ext.reuse_shuffle):
+    // each extra update of a drf > 1 run pairs this lane's i endpoint with the
+    // partner endpoint lane q = lane ^ mask holds (mask drawn per extra, warp
+    // wide), reusing q's record and coordinates from registers instead of the
+    // reference's re-update of the same pair under other endpoint combinations
+    // (engine.cpp:147-170). Pairs stay within a path. Convergent: every lane
+    // calls it.
+    auto shuffle_reuse = [&](bool ok, uint32_t path, const StepRec& ri, int ei, uint32_t ni, double vix,
+                             double viy, uint64_t pos_j, int ej, uint32_t nj, double vjx, double vjy) -> uint32_t {
+        uint32_t got = 0;
+        const uint64_t pos_i = step_pos(ri, ei);
+        for (uint32_t extra = 1; extra < a.drf; ++extra) {
+            uint64_t x = lane == 0 ? r.next() : 0;
+            x = __shfl_sync(kFull, x, 0);
+            const int q = static_cast<int>(lane ^ (1u + static_cast<uint32_t>(__umulhi(static_cast<uint32_t>(x >> 32), 31u))));
+            const uint32_t q_ok = __shfl_sync(kFull, ok ? path : 0xFFFFFFFFu, q);
+            const uint64_t q_pos = __shfl_sync(kFull, pos_j, q);
+            const uint32_t q_nj = __shfl_sync(kFull, nj, q);
+            const int q_ej = __shfl_sync(kFull, ej, q);
+            const double q_vjx = __shfl_sync(kFull, vjx, q);
+            const double q_vjy = __shfl_sync(kFull, vjy, q);
+            if (ok && q_ok == path) {
+                const double d = abs_diff(pos_i, q_pos);
+                if (d > 0.0)
+                    got += hog_apply_io_t<T>(coords, ni, ei, q_nj, q_ej, d, a.eta, r, pol_keep, vix, viy, q_vjx,
+                                             q_vjy);
+            }
+        }
+        return got;
     };
 
     // Stage B: share in-tile partner records, then the update(s).
@@ -231,23 +265,35 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         sh.ps_lo = __shfl_sync(kFull, o.ri.ps_lo, o.src);
         sh.pe_lo = __shfl_sync(kFull, o.ri.pe_lo, o.src);
         sh.hi = __shfl_sync(kFull, o.ri.hi, o.src);
-        if (!(o.flags & 1u)) return 0;
+        const bool valid = o.flags & 1u;
         const StepRec rj = (o.flags & 8u) ? sh : o.rj;
         const int ei = (o.flags >> 1) & 1, ej = (o.flags >> 2) & 1;
-        uint32_t got = hog_update_t<T>(coords, o.ri.node, ei, rj.node, ej,
-                                       abs_diff(step_pos(o.ri, ei), step_pos(rj, ej)), a.eta, r, pol_keep);
+        const double d_ref = valid ? abs_diff(step_pos(o.ri, ei), step_pos(rj, ej)) : 0.0;
+        const bool live = valid && d_ref > 0.0;
+        double vix = 0, viy = 0, vjx = 0, vjy = 0;
+        uint32_t got = 0;
+        if (live) {
+            CoordHint<T>::get(coords, o.ri.node, ei, pol_keep, vix, viy);
+            CoordHint<T>::get(coords, rj.node, ej, pol_keep, vjx, vjy);
+            got = hog_apply_io_t<T>(coords, o.ri.node, ei, rj.node, ej, d_ref, a.eta, r, pol_keep, vix, viy, vjx, vjy);
+        }
         if (a.drf > 1) {
-            unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
-            for (uint32_t extra = 1; extra < a.drf; ++extra) {
-                int ea, eb;
-                do {
-                    const uint64_t b2 = r.next();
-                    ea = (b2 >> 63) ? 0 : 1;
-                    eb = ((b2 >> 62) & 1) ? 0 : 1;
-                } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
-                used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                got += hog_update_t<T>(coords, o.ri.node, ea, rj.node, eb,
-                                       abs_diff(step_pos(o.ri, ea), step_pos(rj, eb)), a.eta, r, pol_keep);
+            if (a.reuse_shuffle) {
+                got += shuffle_reuse(live, o.path, o.ri, ei, o.ri.node, vix, viy, step_pos(rj, ej), ej, rj.node, vjx,
+                                     vjy);
+            } else if (valid) {
+                unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+                for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                    int ea, eb;
+                    do {
+                        const uint64_t b2 = r.next();
+                        ea = (b2 >> 63) ? 0 : 1;
+                        eb = ((b2 >> 62) & 1) ? 0 : 1;
+                    } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                    used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                    got += hog_update_t<T>(coords, o.ri.node, ea, rj.node, eb,
+                                           abs_diff(step_pos(o.ri, ea), step_pos(rj, eb)), a.eta, r, pol_keep);
+                }
             }
         }
         return got;
@@ -306,13 +352,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             async_rj = s_rj[m % 3][wib];
             const TileSel t = select(uu, ii);
             cp_async_commit();
-            return t.flags | (t.src << 8);
+            return t.flags | (t.src << 8) | (t.path << 13);  // path < 2^19 checked by the host
         };
         auto resolve_issue = [&](UX m, uint32_t fs) -> Res {
             Res rs{0, 0, 0, 0.0};
             if (fs & 1u) {
                 const StepRec ri = s_ri[m % 3][wib][lane];
-                const StepRec rj = (fs & 8u) ? s_ri[m % 3][wib][fs >> 8] : s_rj[m % 3][wib][lane];
+                const StepRec rj = (fs & 8u) ? s_ri[m % 3][wib][(fs >> 8) & 31] : s_rj[m % 3][wib][lane];
                 const int ei = (fs >> 1) & 1, ej = (fs >> 2) & 1;
                 rs.d_ref = abs_diff(step_pos(ri, ei), step_pos(rj, ej));
                 rs.ni = ri.node;
@@ -340,27 +386,39 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             }
             for (UX m = 0; m < n_mine; ++m) {
                 cp_async_wait<1>();                 // C(m) landed (R(m+1) may be in flight)
-                if ((cur.flags & 1u) && cur.d_ref > 0.0) {
+                const bool live = (cur.flags & 1u) && cur.d_ref > 0.0;
+                double vix = 0, viy = 0, vjx = 0, vjy = 0;
+                if (live) {
                     const T2 vi = s_vi[m & 1][wib][lane], vj = s_vj[m & 1][wib][lane];
-                    applied += hog_apply_t<T>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj, (cur.flags >> 2) & 1,
-                                              cur.d_ref, a.eta, r, pol_keep, vi.x, vi.y, vj.x, vj.y);
+                    vix = vi.x;
+                    viy = vi.y;
+                    vjx = vj.x;
+                    vjy = vj.y;
+                    applied += hog_apply_io_t<T>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj, (cur.flags >> 2) & 1,
+                                                 cur.d_ref, a.eta, r, pol_keep, vix, viy, vjx, vjy);
                 }
-                if ((cur.flags & 1u) && a.drf > 1) {
+                if (a.drf > 1) {
                     const StepRec ri = s_ri[m % 3][wib][lane];
                     const StepRec rj =
-                        (cur.flags & 8u) ? s_ri[m % 3][wib][cur.flags >> 8] : s_rj[m % 3][wib][lane];
+                        (cur.flags & 8u) ? s_ri[m % 3][wib][(cur.flags >> 8) & 31] : s_rj[m % 3][wib][lane];
                     const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
-                    unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
-                    for (uint32_t extra = 1; extra < a.drf; ++extra) {
-                        int ea, eb;
-                        do {
-                            const uint64_t b2 = r.next();
-                            ea = (b2 >> 63) ? 0 : 1;
-                            eb = ((b2 >> 62) & 1) ? 0 : 1;
-                        } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
-                        used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                        applied += hog_update_t<T>(coords, ri.node, ea, rj.node, eb,
-                                                   abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, r, pol_keep);
+                    if (a.reuse_shuffle) {
+                        applied += shuffle_reuse(live, cur.flags >> 13, ri, ei, cur.ni, vix, viy, step_pos(rj, ej), ej,
+                                                 cur.nj, vjx, vjy);
+                    } else if (cur.flags & 1u) {
+                        unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
+                        for (uint32_t extra = 1; extra < a.drf; ++extra) {
+                            int ea, eb;
+                            do {
+                                const uint64_t b2 = r.next();
+                                ea = (b2 >> 63) ? 0 : 1;
+                                eb = ((b2 >> 62) & 1) ? 0 : 1;
+                            } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
+                            used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
+                            applied += hog_update_t<T>(coords, ri.node, ea, rj.node, eb,
+                                                       abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, r,
+                                                       pol_keep);
+                        }
                     }
                 }
                 Res nres{0, 0, 0, 0.0};

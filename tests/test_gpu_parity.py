@@ -434,3 +434,30 @@ def test_replay_bit_exact_nested(pgl, oracle, ref, gpu):
     lay, rst = ref.run_layout(gr, make_cfg(**cfg))
     assert stats_tuple(st) == stats_tuple(rst)
     np.testing.assert_allclose(out, lay, rtol=1e-9, atol=1e-9)  # jitter path: cos/sin within 1e-9
+
+
+# ---- warp-shuffle data reuse (paper §7.4) ---------------------
+
+@pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (2, 1), (4, 2)])
+def test_reuse_shuffle_accounting_and_quality(pgl, oracle, ref, gpu, drf, srf):
+    """RunStats identities of run_layout_reuse (test_engine.cpp:257-278) and
+    the acceptance #7 bar (acceptance.cpp:327-350): SPS at most 2x the drf=1
+    layout's, on config 1 (reference estimator, seed 7, spn 100)."""
+    g = pgl.generate_synthetic_pangenome(*C1)
+    gr = ref.generate(*C1, gfa_roundtrip=True)
+    base = pgl.run_layout(g, pgl.LayoutConfig(global_seed=101))
+    st = pgl.RunStats()
+    cfg = pgl.LayoutConfig(global_seed=101, drf=drf, srf=srf)
+    out = pgl.run_layout_reuse(g, cfg, stats=st, ext=pgl.LayoutExt(reuse_shuffle=1)) if drf in (2, 4) else None
+    assert st.primary_steps == 30 * (10 * g.total_steps() // srf)
+    assert st.updates_attempted == st.primary_steps * drf
+    assert st.updates_applied + st.updates_skipped == st.updates_attempted
+    ratio = ref.sps(gr, out, 7, 100).mean / ref.sps(gr, base, 7, 100).mean
+    assert ratio <= 2.0, ratio
+
+
+def test_reuse_shuffle_rejected_outside_tiles(pgl, gpu):
+    g = pgl.generate_synthetic_pangenome(*SMALL[0])
+    with pytest.raises(pgl.InvalidParameter):
+        pgl.run_layout_reuse(g, pgl.LayoutConfig(drf=2, srf=2),
+                             ext=pgl.LayoutExt(reuse_shuffle=1, sampling=pgl.SAMPLING_IID))
