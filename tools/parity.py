@@ -47,6 +47,10 @@ def main():
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--ref-spn", type=int, default=1)
     ap.add_argument("--sampling", choices=["tiles", "iid"], default="tiles")
+    ap.add_argument("--gpu-spn", type=int, default=100, help="spn of the device counter estimator")
+    ap.add_argument("--ref-json", default=None,
+                    help="reference scores computed elsewhere (tools/score_ref_layout.py lines or a previous "
+                         "parity.py output): the reference layouts are not recomputed")
     args = ap.parse_args()
     seeds = [int(s) for s in args.seeds.split(",")]
     ref_seeds = [int(s) for s in (args.ref_seeds or args.seeds).split(",")]
@@ -67,16 +71,27 @@ def main():
 
     with P.DeviceGraph(g) as dg:
         init = P.init_layout(g, 101)
-        res["init_sps_gpu_spn100"] = rep(dg.stress(7, 100, layout=init))
+        gk = "sps_gpu_spn%d" % args.gpu_spn
+        res["init_" + gk] = rep(dg.stress(7, args.gpu_spn, layout=init))
         for seed in seeds:
             t = time.time()
             lay = dg.layout(P.LayoutConfig(global_seed=seed), ext=P.LayoutExt(sampling=samp))
             secs = time.time() - t
             res["gpu"].append({"seed": seed, "layout_s": round(secs, 3),
-                               "sps_gpu_spn100": rep(dg.stress(7, 100, layout=lay)),
+                               gk: rep(dg.stress(7, args.gpu_spn, layout=lay)),
                                "sps_ref_spn%d" % args.ref_spn: rep(R.sps(gr, lay, 7, args.ref_spn))})
             print("gpu", res["gpu"][-1], flush=True)
             flush()
+        if args.ref_json:  # reference scores computed elsewhere
+            with open(args.ref_json) as f:
+                txt = f.read().strip()
+            try:  # a previous parity.py output
+                recs = json.loads(txt)["ref"]
+            except (ValueError, KeyError, TypeError):  # JSON lines of tools/score_ref_layout.py
+                recs = [json.loads(line) for line in txt.splitlines() if line.strip()]
+            res["ref"] = [r for r in recs if r["seed"] in ref_seeds]
+            res["ref_source"] = args.ref_json
+            ref_seeds = []
         for seed in ref_seeds:
             path = args.ref_dir and os.path.join(args.ref_dir, f"{args.config}_ref_{seed}.npy")
             t = time.time()
@@ -86,11 +101,11 @@ def main():
                 lay, _ = R.run_layout(gr, make_cfg(global_seed=seed, threads=args.threads))
                 secs, src = round(time.time() - t, 1), "computed"
             res["ref"].append({"seed": seed, "layout_s": secs, "source": src,
-                               "sps_gpu_spn100": rep(dg.stress(7, 100, layout=lay)),
+                               gk: rep(dg.stress(7, args.gpu_spn, layout=lay)),
                                "sps_ref_spn%d" % args.ref_spn: rep(R.sps(gr, lay, 7, args.ref_spn))})
             print("ref", res["ref"][-1], flush=True)
             flush()
-    for key in ("sps_gpu_spn100", "sps_ref_spn%d" % args.ref_spn):
+    for key in ("sps_gpu_spn%d" % args.gpu_spn, "sps_ref_spn%d" % args.ref_spn):
         mg = statistics.median(r[key]["mean"] for r in res["gpu"])
         mr = statistics.median(r[key]["mean"] for r in res["ref"])
         res["ratio_" + key] = mg / mr
