@@ -114,6 +114,7 @@ struct LaunchShape {
     int threads = 256;
     int variant = 0;
     bool idx32 = false;  // tile kernel: 32-bit index instantiation
+    size_t smem = 0;     // dynamic shared memory per CTA
 };
 
 // Occupancy-derived persistent grid for the Hogwild kernel.

@@ -53,6 +53,20 @@ __device__ __forceinline__ uint32_t path_of_step(const DevGraph& g, uint64_t i) 
 
 // Stage A product for one lane: its step i (record in flight), its partner j
 // (record in flight when outside the unit) and the coins.
+struct AsyncRes {  // async pipeline: a resolved update, waiting for its endpoints
+    uint32_t ni, nj, flags, _pad;
+    double d_ref;
+};
+
+// shared memory of the async pipeline with lookahead L, 256-thread blocks
+template <typename T>
+constexpr size_t async_smem_bytes(int L) {
+    using T2 = std::conditional_t<std::is_same_v<T, double>, double2, float2>;
+    return L == 0 ? 0
+                  : static_cast<size_t>(8 * 32) *
+                        ((2 * L + 1) * (2 * sizeof(StepRec) + sizeof(uint32_t)) + (L + 1) * (2 * sizeof(T2) + sizeof(AsyncRes)));
+}
+
 struct TileSel {
     StepRec ri, rj;       // rj valid when !(flags & 8)
     uint32_t src;         // lane holding j's record when in-tile
@@ -67,7 +81,7 @@ struct TileSel {
 //   asynchronous (kAsync = true): records and endpoints are copied global ->
 //     shared with cp.async (no registers held while in flight), three units in
 //     flight: endpoints of m landing, records of m+1 landing, m+2 selected.
-template <typename T, int kMinBlocks, bool kAsync, bool k32>
+template <typename T, int kMinBlocks, int kAsync, bool k32>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                 DevStats* stats, IterArgs a) {
     // k32: every step index, unit index and path length fits in 31 bits
@@ -314,7 +328,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
         if (ii >= S) ii -= S;
     };
-    if constexpr (!kAsync) {
+    if constexpr (kAsync == 0) {
         if (n_mine) {
             TileSel cur = select(u, i0);
             for (UX m = 0; m < n_mine; ++m) {
@@ -331,65 +345,42 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
     } else {
         // Asynchronous pipeline: records and endpoints travel global ->
-        // shared by cp.async (no registers held while in flight). Round m:
-        //   1. wait for the endpoints of unit m, apply its update;
-        //   2. wait for the records of unit m+1, resolve its partner (own
-        //      copy, or the in-tile owner's slot), issue its endpoint copies;
-        //   3. select unit m+2, issue its record copies.
-        // Commit order ..., C(m), R(m+1), C(m+1), R(m+2): "wait_group 1"
-        // leaves only the newest group in flight.
+        // shared by cp.async (no registers held while in flight); the
+        // per-unit state between stages lives in shared memory too. With
+        // lookahead L = kAsync, round t
+        //   1. waits for the endpoints of unit t and applies its update;
+        //   2. waits for the records of unit t+L, resolves its partner (own
+        //      copy, or the in-tile owner's slot) and issues its endpoint
+        //      copies (group C(t+L));
+        //   3. selects unit t+2L and issues its record copies (group R(t+2L)).
+        // Every round commits exactly two groups (C, then R, possibly empty),
+        // so C(t) has 2L-1 newer groups when step 1 waits and R(t+L) has
+        // 2L-2 when step 2 waits.
+        constexpr int L = kAsync;
+        constexpr int kRS = 2 * L + 1;  // record / selection slots
+        constexpr int kCS = L + 1;      // endpoint / resolved slots
         using T2 = std::conditional_t<std::is_same_v<T, double>, double2, float2>;
         constexpr int kWarps = 8;  // 256-thread blocks
-        __shared__ StepRec s_ri[3][kWarps][32], s_rj[3][kWarps][32];
-        __shared__ T2 s_vi[2][kWarps][32], s_vj[2][kWarps][32];
+        // dynamic shared memory (async_smem_bytes): [kRS] record pairs and
+        // selection flags, [kCS] endpoint pairs and resolved updates
+        extern __shared__ __align__(16) unsigned char dyn_smem[];
+        auto* s_ri = reinterpret_cast<StepRec(*)[kWarps][32]>(dyn_smem);
+        auto* s_rj = s_ri + kRS;
+        auto* s_vi = reinterpret_cast<T2(*)[kWarps][32]>(s_rj + kRS);
+        auto* s_vj = s_vi + kCS;
+        auto* s_res = reinterpret_cast<AsyncRes(*)[kWarps][32]>(s_vj + kCS);
+        auto* s_fl = reinterpret_cast<uint32_t(*)[kWarps][32]>(s_res + kCS);
         const int wib = static_cast<int>(threadIdx.x >> 5);
-        struct Res {  // a resolved update, waiting for its endpoints
-            uint32_t ni, nj, flags;
-            double d_ref;
-        };
-        auto issue_sel = [&](UX m, UX uu, UX ii) -> uint32_t {
-            async_ri = s_ri[m % 3][wib];
-            async_rj = s_rj[m % 3][wib];
-            const TileSel t = select(uu, ii);
-            cp_async_commit();
-            return t.flags | (t.src << 8) | (t.path << 13);  // path < 2^19 checked by the host
-        };
-        auto resolve_issue = [&](UX m, uint32_t fs) -> Res {
-            Res rs{0, 0, 0, 0.0};
-            if (fs & 1u) {
-                const StepRec ri = s_ri[m % 3][wib][lane];
-                const StepRec rj = (fs & 8u) ? s_ri[m % 3][wib][(fs >> 8) & 31] : s_rj[m % 3][wib][lane];
-                const int ei = (fs >> 1) & 1, ej = (fs >> 2) & 1;
-                rs.d_ref = abs_diff(step_pos(ri, ei), step_pos(rj, ej));
-                rs.ni = ri.node;
-                rs.nj = rj.node;
-                rs.flags = fs;
-                if (rs.d_ref > 0.0) {
-                    cp_async<sizeof(T2)>(&s_vi[m & 1][wib][lane], coord_addr<T>(coords, ri.node, ei), pol_keep);
-                    cp_async<sizeof(T2)>(&s_vj[m & 1][wib][lane], coord_addr<T>(coords, rj.node, ej), pol_keep);
-                }
-            }
-            cp_async_commit();
-            return rs;
-        };
-        if (n_mine) {
-            uint32_t f_next = issue_sel(0, u, i0);  // R(0)
-            cp_async_wait<0>();
-            __syncwarp();
-            Res cur = resolve_issue(0, f_next);     // C(0)
-            f_next = 0;
-            if (n_mine > 1) {
-                advance(u, i0);
-                f_next = issue_sel(1, u, i0);       // R(1)
-            } else {
-                cp_async_commit();
-            }
-            for (UX m = 0; m < n_mine; ++m) {
-                cp_async_wait<1>();                 // C(m) landed (R(m+1) may be in flight)
+        const int64_t N = static_cast<int64_t>(n_mine);
+        for (int64_t t = -2 * L; t < N; ++t) {
+            if (t >= 0) {  // 1. apply unit t
+                cp_async_wait<2 * L - 1>();
+                const int cs = static_cast<int>(t % kCS), rs = static_cast<int>(t % kRS);
+                const AsyncRes cur = s_res[cs][wib][lane];
                 const bool live = (cur.flags & 1u) && cur.d_ref > 0.0;
                 double vix = 0, viy = 0, vjx = 0, vjy = 0;
                 if (live) {
-                    const T2 vi = s_vi[m & 1][wib][lane], vj = s_vj[m & 1][wib][lane];
+                    const T2 vi = s_vi[cs][wib][lane], vj = s_vj[cs][wib][lane];
                     vix = vi.x;
                     viy = vi.y;
                     vjx = vj.x;
@@ -398,9 +389,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                                                  cur.d_ref, a.eta, r, pol_keep, vix, viy, vjx, vjy);
                 }
                 if (a.drf > 1) {
-                    const StepRec ri = s_ri[m % 3][wib][lane];
-                    const StepRec rj =
-                        (cur.flags & 8u) ? s_ri[m % 3][wib][(cur.flags >> 8) & 31] : s_rj[m % 3][wib][lane];
+                    const StepRec ri = s_ri[rs][wib][lane];
+                    const StepRec rj = (cur.flags & 8u) ? s_ri[rs][wib][(cur.flags >> 8) & 31] : s_rj[rs][wib][lane];
                     const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
                     if (a.reuse_shuffle) {
                         applied += shuffle_reuse(live, cur.flags >> 13, ri, ei, cur.ni, vix, viy, step_pos(rj, ej), ej,
@@ -421,22 +411,41 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                         }
                     }
                 }
-                Res nres{0, 0, 0, 0.0};
-                if (m + 1 < n_mine) {
-                    cp_async_wait<0>();             // R(m+1) landed
-                    __syncwarp();                   // in-tile partners read other lanes' copies
-                    nres = resolve_issue(m + 1, f_next);  // C(m+1)
-                    f_next = 0;
-                    if (m + 2 < n_mine) {
-                        advance(u, i0);
-                        f_next = issue_sel(m + 2, u, i0);  // R(m+2)
-                    } else {
-                        cp_async_commit();
+            }
+            const int64_t tr = t + L;  // 2. resolve unit t+L, issue its endpoint copies
+            if (tr >= 0 && tr < N) {
+                cp_async_wait<2 * L - 2>();
+                __syncwarp();  // in-tile partners read other lanes' copies
+                const int cs = static_cast<int>(tr % kCS), rs = static_cast<int>(tr % kRS);
+                const uint32_t fs = s_fl[rs][wib][lane];
+                AsyncRes res{0, 0, 0, 0, 0.0};
+                if (fs & 1u) {
+                    const StepRec ri = s_ri[rs][wib][lane];
+                    const StepRec rj = (fs & 8u) ? s_ri[rs][wib][(fs >> 8) & 31] : s_rj[rs][wib][lane];
+                    const int ei = (fs >> 1) & 1, ej = (fs >> 2) & 1;
+                    res.d_ref = abs_diff(step_pos(ri, ei), step_pos(rj, ej));
+                    res.ni = ri.node;
+                    res.nj = rj.node;
+                    res.flags = fs;
+                    if (res.d_ref > 0.0) {
+                        cp_async<sizeof(T2)>(&s_vi[cs][wib][lane], coord_addr<T>(coords, ri.node, ei), pol_keep);
+                        cp_async<sizeof(T2)>(&s_vj[cs][wib][lane], coord_addr<T>(coords, rj.node, ej), pol_keep);
                     }
                 }
-                __syncwarp();  // slot reuse: every lane is done with unit m's shared data
-                cur = nres;
+                s_res[cs][wib][lane] = res;
             }
+            cp_async_commit();
+            const int64_t ts = t + 2 * L;  // 3. select unit t+2L, issue its record copies
+            if (ts < N) {
+                if (ts > 0) advance(u, i0);
+                const int rs = static_cast<int>(ts % kRS);
+                async_ri = s_ri[rs][wib];
+                async_rj = s_rj[rs][wib];
+                const TileSel sel = select(u, i0);
+                s_fl[rs][wib][lane] = sel.flags | (sel.src << 8) | (sel.path << 13);  // path < 2^19 (host check)
+            }
+            cp_async_commit();
+            __syncwarp();  // slot reuse: every lane is done with this round's shared data
         }
     }
 
@@ -459,20 +468,28 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 //   5  asynchronous pipeline, 4 CTAs/SM (64 registers)
 //   6  asynchronous pipeline, 3 CTAs/SM; auto once the graph fills the GPU
 //      (config 2: 43 G upd/s vs 39 for variant 1)
+//   8  asynchronous pipeline with two units of lookahead per stage (five
+//      units in flight per warp), 2 CTAs/SM (88 KB of shared memory per CTA)
 // (3 and 4 were a three-stage register pipeline and a bulk-L2-prefetch
 // four-stage pipeline; measured no better, removed.) Bit 4 forces the
 // 64-bit index instantiation (measurements).
 template <typename T, bool k32>
 const void* tiles_fn_t(int variant) {
-    return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, false, k32>)
-           : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, true, k32>)
-           : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, true, k32>)
-                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, false, k32>);
+    return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
+           : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
+           : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 1, k32>)
+           : variant == 8 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 2, 2, k32>)
+                          : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 0, k32>);
 }
 
 template <typename T>
 const void* tiles_fn(int variant, bool k32) {
     return k32 ? tiles_fn_t<T, true>(variant) : tiles_fn_t<T, false>(variant);
+}
+
+template <typename T>
+size_t tiles_smem(int variant) {
+    return async_smem_bytes<T>(variant == 5 || variant == 6 ? 1 : variant == 8 ? 2 : 0);
 }
 
 }  // namespace
@@ -485,11 +502,15 @@ LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block
     sh.idx32 = total_steps < (1ULL << 30) && !(variant & 16);
     variant &= 15;
     sh.variant = variant;
-    sh.threads = block_threads > 0 ? block_threads : 256;
+    sh.smem = coord_f64 ? tiles_smem<double>(variant) : tiles_smem<float>(variant);
+    // the async pipeline's shared-memory layout assumes 256-thread blocks
+    sh.threads = sh.smem ? 256 : (block_threads > 0 ? block_threads : 256);
+    const void* fn = coord_f64 ? tiles_fn<double>(variant, sh.idx32) : tiles_fn<float>(variant, sh.idx32);
+    if (sh.smem)
+        PGL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem)));
     int sms = 0, occ = 0;
     PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, coord_f64 ? tiles_fn<double>(variant, sh.idx32) : tiles_fn<float>(variant, sh.idx32), sh.threads, 0));
+    PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, sh.threads, sh.smem));
     if (occ < 1) occ = 1;
     uint64_t warps = static_cast<uint64_t>(sms) * occ * (sh.threads / 32);
     if (max_warps && warps > max_warps) warps = max_warps;
@@ -502,7 +523,8 @@ void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_f64, DevRng rng
                       const IterArgs& a, LaunchShape shape, void* stream) {
     void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
     PGL_CUDA(cudaLaunchKernel(coord_f64 ? tiles_fn<double>(shape.variant, shape.idx32) : tiles_fn<float>(shape.variant, shape.idx32),
-                              dim3(shape.blocks), dim3(shape.threads), args, 0, static_cast<cudaStream_t>(stream)));
+                              dim3(shape.blocks), dim3(shape.threads), args, shape.smem,
+                              static_cast<cudaStream_t>(stream)));
 }
 
 }  // namespace pgl
