@@ -579,8 +579,8 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
         PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         v = cap >= static_cast<uint32_t>(sms) * 3 * 8 ? 6 : 1;
     }
-    if (v != 1 && v != 2 && v != 5 && v != 6 && v != 8)
-        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5, 6, 8");
+    if (v != 1 && v != 2 && v != 5 && v != 6)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5, 6");
     return v | force64;
 }
 

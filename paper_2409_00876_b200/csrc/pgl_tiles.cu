@@ -468,8 +468,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 //   5  asynchronous pipeline, 4 CTAs/SM (64 registers)
 //   6  asynchronous pipeline, 3 CTAs/SM; auto once the graph fills the GPU
 //      (config 2: 43 G upd/s vs 39 for variant 1)
-//   8  asynchronous pipeline with two units of lookahead per stage (five
-//      units in flight per warp), 2 CTAs/SM (88 KB of shared memory per CTA)
+// (A lookahead of two units per stage -- five units in flight per warp, 88 KB
+// of shared memory per CTA, 2 CTAs/SM -- measured 20% slower than variant 6.)
 // (3 and 4 were a three-stage register pipeline and a bulk-L2-prefetch
 // four-stage pipeline; measured no better, removed.) Bit 4 forces the
 // 64-bit index instantiation (measurements).
@@ -478,7 +478,6 @@ const void* tiles_fn_t(int variant) {
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
            : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 1, k32>)
-           : variant == 8 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 2, 2, k32>)
                           : reinterpret_cast<const void*>(k_sgd_tiles<T, 1, 0, k32>);
 }
 
@@ -489,7 +488,7 @@ const void* tiles_fn(int variant, bool k32) {
 
 template <typename T>
 size_t tiles_smem(int variant) {
-    return async_smem_bytes<T>(variant == 5 || variant == 6 ? 1 : variant == 8 ? 2 : 0);
+    return async_smem_bytes<T>(variant == 5 || variant == 6 ? 1 : 0);
 }
 
 }  // namespace
