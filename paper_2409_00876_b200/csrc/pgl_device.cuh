@@ -54,6 +54,43 @@ __host__ __device__ __forceinline__ void seed_worker(uint64_t seed, uint64_t wor
     if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = kPhi;
 }
 
+// xoshiro256 with a draw counter (the speculative replay producer checks how
+// many draws a step consumed).
+struct XoCount {
+    Xo r;
+    uint32_t n = 0;
+    __device__ __forceinline__ uint64_t next() {
+        ++n;
+        return r.next();
+    }
+    __device__ __forceinline__ double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    __device__ __forceinline__ bool coin() { return (next() >> 63) != 0; }
+    __device__ __forceinline__ uint64_t below(uint64_t n_) { return __umul64hi(next(), n_); }
+};
+
+// s := M s over GF(2)^256; M column-major, [256][4] u64 (xoshiro's state
+// transition is linear, so a power of it jumps the stream ahead).
+__device__ __forceinline__ void gf2_apply(uint64_t s[4], const uint64_t* __restrict__ M) {
+    uint64_t y0 = 0, y1 = 0, y2 = 0, y3 = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        uint64_t x = s[w];
+        while (x) {
+            const int b = __ffsll(static_cast<long long>(x)) - 1;
+            x &= x - 1;
+            const uint64_t* c = M + (static_cast<uint64_t>(w) * 64 + b) * 4;
+            y0 ^= __ldg(c);
+            y1 ^= __ldg(c + 1);
+            y2 ^= __ldg(c + 2);
+            y3 ^= __ldg(c + 3);
+        }
+    }
+    s[0] = y0;
+    s[1] = y1;
+    s[2] = y2;
+    s[3] = y3;
+}
+
 // ---- Zipf by rejection inversion (rng.hpp:103-144) ------------------------
 
 __device__ __forceinline__ double zipf_helper1(double x) {
@@ -75,7 +112,8 @@ __device__ __forceinline__ double zipf_Hinv(double theta, double x) {
     return exp(zipf_helper1(t) * x);
 }
 
-__device__ __forceinline__ uint64_t zipf_sample(const PathConst& pc, double theta, Xo& r) {
+template <typename R>
+__device__ __forceinline__ uint64_t zipf_sample(const PathConst& pc, double theta, R& r) {
     if (pc.zn == 1) return 1;
     for (;;) {
         const double u = pc.hxn + r.uniform() * (pc.hx1 - pc.hxn);

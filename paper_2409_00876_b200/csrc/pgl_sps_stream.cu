@@ -70,33 +70,12 @@ struct PathInfo {
     uint64_t n_chunks;
 };
 
-__device__ __forceinline__ void jump(uint64_t s[4], const uint64_t* __restrict__ M) {
-    uint64_t y0 = 0, y1 = 0, y2 = 0, y3 = 0;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        uint64_t x = s[w];
-        while (x) {
-            const int b = __ffsll(static_cast<long long>(x)) - 1;
-            x &= x - 1;
-            const uint64_t* c = M + (static_cast<uint64_t>(w) * 64 + b) * 4;
-            y0 ^= __ldg(c);
-            y1 ^= __ldg(c + 1);
-            y2 ^= __ldg(c + 2);
-            y3 ^= __ldg(c + 3);
-        }
-    }
-    s[0] = y0;
-    s[1] = y1;
-    s[2] = y2;
-    s[3] = y3;
-}
-
 // stream state of path p at draw index c * D
 __device__ Xo chunk_state(uint64_t seed, uint32_t p, uint64_t c, const uint64_t* __restrict__ jumps) {
     uint64_t s[4];
     seed_worker(seed, kStreamSps + p, s);
     for (int k = 0; c; ++k, c >>= 1)
-        if (c & 1) jump(s, jumps + static_cast<uint64_t>(k) * 256 * 4);
+        if (c & 1) gf2_apply(s, jumps + static_cast<uint64_t>(k) * 256 * 4);
     return Xo{s[0], s[1], s[2], s[3]};
 }
 
