@@ -54,20 +54,6 @@ __host__ __device__ __forceinline__ void seed_worker(uint64_t seed, uint64_t wor
     if ((s[0] | s[1] | s[2] | s[3]) == 0) s[0] = kPhi;
 }
 
-// xoshiro256 with a draw counter (the speculative replay producer checks how
-// many draws a step consumed).
-struct XoCount {
-    Xo r;
-    uint32_t n = 0;
-    __device__ __forceinline__ uint64_t next() {
-        ++n;
-        return r.next();
-    }
-    __device__ __forceinline__ double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
-    __device__ __forceinline__ bool coin() { return (next() >> 63) != 0; }
-    __device__ __forceinline__ uint64_t below(uint64_t n_) { return __umul64hi(next(), n_); }
-};
-
 // s := M s over GF(2)^256; M column-major, [256][4] u64 (xoshiro's state
 // transition is linear, so a power of it jumps the stream ahead).
 __device__ __forceinline__ void gf2_apply(uint64_t s[4], const uint64_t* __restrict__ M) {

@@ -13,10 +13,6 @@
 // across two warps instead.
 #include <cuda_runtime.h>
 
-#include <mutex>
-#include <type_traits>
-#include <vector>
-
 #include "pgl_device.cuh"
 
 namespace pgl {
@@ -34,14 +30,13 @@ struct Plan {
     bool cooling;  // cooling flag in force for this step
 };
 
-// select_step_pair (engine.cpp:52-80), the two coins (:137-138) and the
-// coins of the drf extra combinations (:155-161) under a known cooling flag.
-// R is Xo, or XoCount when the caller needs the number of draws.
-template <typename R>
-__device__ __forceinline__ Plan plan_known(const DevGraph& g, const IterArgs& a, R& r, bool cooling,
-                                           bool load_records) {
+// Batch decision (engine.cpp:115-124), select_step_pair (:52-80), the two
+// coins (:137-138) and the coins of the drf extra combinations (:155-161).
+__device__ __forceinline__ Plan plan_step(const DevGraph& g, const IterArgs& a, uint64_t s, Xo r, bool& cooling,
+                                          bool load_records = true) {
     Plan P;
-    P.opened = false;
+    P.opened = (s % a.batch) == 0;
+    if (P.opened) cooling = a.force_cooling || r.coin();
     P.cooling = cooling;
     P.valid = false;
     P.ei = P.ej = 0;
@@ -87,10 +82,7 @@ __device__ __forceinline__ Plan plan_known(const DevGraph& g, const IterArgs& a,
             P.ej = r.coin() ? 0 : 1;
         }
     }
-    if constexpr (std::is_same_v<R, Xo>)
-        P.r_mid = r;
-    else
-        P.r_mid = r.r;
+    P.r_mid = r;
     if (P.valid && a.drf > 1) {
         unsigned used = 1u << ((P.ei ? 2 : 0) | (P.ej ? 1 : 0));
         for (uint32_t extra = 1; extra < a.drf; ++extra) {
@@ -102,20 +94,7 @@ __device__ __forceinline__ Plan plan_known(const DevGraph& g, const IterArgs& a,
             used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
         }
     }
-    if constexpr (std::is_same_v<R, Xo>)
-        P.r_end = r;
-    else
-        P.r_end = r.r;
-    return P;
-}
-
-// Batch decision (engine.cpp:115-124) then plan_known.
-__device__ __forceinline__ Plan plan_step(const DevGraph& g, const IterArgs& a, uint64_t s, Xo r, bool& cooling,
-                                          bool load_records = true) {
-    const bool opened = (s % a.batch) == 0;
-    if (opened) cooling = a.force_cooling || r.coin();
-    Plan P = plan_known(g, a, r, cooling, load_records);
-    P.opened = opened;
+    P.r_end = r;
     return P;
 }
 
@@ -211,8 +190,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 }
 
 __global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __restrict__ gcoords, uint64_t* rng4,
-                                                      DevStats* stats, IterArgs a, int use_smem,
-                                                      const uint64_t* __restrict__ jumps) {
+                                                      DevStats* stats, IterArgs a, int use_smem) {
     extern __shared__ __align__(16) unsigned char smem[];
     Slot* ring = reinterpret_cast<Slot*>(smem);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kRing * sizeof(Slot));
@@ -235,86 +213,47 @@ __global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __rest
     __syncthreads();
     volatile ReplayCtl* vc = ctl;
 
-    if (threadIdx.x < 32) {  // ---------------- producer (warp 0) ----------------
-        // Speculative lane-parallel planning. A round covers up to 32 steps of
-        // one batch (the batch coin, if any, is drawn first). A regular step
-        // consumes c = 5 draws when cooling (pick, Zipf accepted at the first
-        // try, sign, two coins) or 4 when not (pick, partner, two coins), so
-        // lane t plans step s0 + t from the stream jumped ahead by t*c draws
-        // (jumps[c - 4][t] = T^(t*c), T = xoshiro's GF(2) transition). Every
-        // plan up to and including the first irregular one (a Zipf
-        // rejection, a collision redraw, a skipped step) started from the
-        // right stream position and is kept; the next round starts after it.
-        // drf > 1 (coin pairs until an unused combination) plans one step
-        // per round.
-        const uint32_t lane = threadIdx.x;
+    if (threadIdx.x == 0) {  // ---------------- producer ----------------
         Xo r{rng4[0], rng4[1], rng4[2], rng4[3]};
         bool cool_state = false;  // engine.cpp:113
         uint32_t epoch = 0;
-        uint64_t s0 = 0, q = 0;
+        uint64_t s = 0, q = 0;
         for (;;) {
-            const uint32_t req = __shfl_sync(0xFFFFFFFFu, lane == 0 ? vc->req_epoch : 0u, 0);
-            if (req != epoch) {  // consumer drew a jitter: replan from its state
+            if (vc->req_epoch != epoch) {  // consumer drew a jitter: replan from its state
                 __threadfence_block();
-                epoch = req;
+                epoch = vc->req_epoch;
                 r = Xo{vc->req_state.a, vc->req_state.b, vc->req_state.c, vc->req_state.d};
-                s0 = vc->req_step;
+                s = vc->req_step;
                 cool_state = vc->req_cool != 0;
             }
-            if (s0 >= a.steps) {
-                if (__shfl_sync(0xFFFFFFFFu, lane == 0 ? vc->done : 0u, 0)) break;
+            if (s >= a.steps) {
+                if (vc->done) break;
                 continue;
             }
-            const unsigned long long tail = __shfl_sync(0xFFFFFFFFull, lane == 0 ? vc->tail : 0ull, 0);
-            if (q + 32 - tail > kRing) continue;  // ring full (re-checks the restart request)
-            // the round: steps s0 .. s0 + m - 1, one batch
-            Xo rb = r;
-            bool cool = cool_state;
-            const uint64_t in_b = s0 % a.batch;
-            const bool opened = in_b == 0;
-            if (opened) cool = a.force_cooling || rb.coin();
-            uint64_t m = a.batch - in_b;
-            if (m > 32) m = 32;
-            if (m > a.steps - s0) m = a.steps - s0;
-            if (a.drf > 1) m = 1;
-            const uint32_t c = cool ? 5u : 4u;
-            Plan P{};
-            bool regular = true;
-            if (lane < m) {
-                uint64_t st[4] = {rb.a, rb.b, rb.c, rb.d};
-                if (lane) gf2_apply(st, jumps + (static_cast<uint64_t>(c - 4) * 32 + lane) * 256 * 4);
-                XoCount rc{Xo{st[0], st[1], st[2], st[3]}, 0};
-                P = plan_known(g, a, rc, cool, /*load_records=*/false);
-                regular = rc.n == c;
+            while (q - vc->tail >= kRing) {  // ring full
+                if (vc->req_epoch != epoch) break;
             }
-            const unsigned irr = __ballot_sync(0xFFFFFFFFu, lane < m && !regular);
-            const uint32_t keep = irr ? static_cast<uint32_t>(__ffs(irr)) : static_cast<uint32_t>(m);  // lanes kept
-            if (lane < keep) {
-                Slot& sl = ring[(q + lane) % kRing];
-                sl.r_mid = P.r_mid;
-                sl.r_end = P.r_end;
-                sl.step = s0 + lane;
-                sl.epoch = epoch;
-                sl.flags = (P.valid ? 1u : 0u) | ((opened && lane == 0) ? 2u : 0u) | (cool ? 4u : 0u) |
-                           (P.ei ? 8u : 0u) | (P.ej ? 16u : 0u);
-                uint64_t* b = bar + ((q + lane) % kRing);
-                if (P.valid) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_arrive_tx(b, 2 * sizeof(StepRec));
-                    tma_load(&sl.ri, g.step + P.gi, sizeof(StepRec), b);
-                    tma_load(&sl.rj, g.step + P.gj, sizeof(StepRec), b);
-                } else {
-                    mbar_arrive(b);
-                }
+            if (q - vc->tail >= kRing) continue;
+            const Plan P = plan_step(g, a, s, r, cool_state, /*load_records=*/false);
+            Slot& sl = ring[q % kRing];
+            sl.r_mid = P.r_mid;
+            sl.r_end = P.r_end;
+            sl.step = s;
+            sl.epoch = epoch;
+            sl.flags = (P.valid ? 1u : 0u) | (P.opened ? 2u : 0u) | (P.cooling ? 4u : 0u) | (P.ei ? 8u : 0u) |
+                       (P.ej ? 16u : 0u);
+            uint64_t* b = bar + (q % kRing);
+            if (P.valid) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(b, 2 * sizeof(StepRec));
+                tma_load(&sl.ri, g.step + P.gi, sizeof(StepRec), b);
+                tma_load(&sl.rj, g.step + P.gj, sizeof(StepRec), b);
+            } else {
+                mbar_arrive(b);
             }
-            // the stream continues after the last kept plan
-            r.a = __shfl_sync(0xFFFFFFFFu, P.r_end.a, keep - 1);
-            r.b = __shfl_sync(0xFFFFFFFFu, P.r_end.b, keep - 1);
-            r.c = __shfl_sync(0xFFFFFFFFu, P.r_end.c, keep - 1);
-            r.d = __shfl_sync(0xFFFFFFFFu, P.r_end.d, keep - 1);
-            cool_state = cool;
-            s0 += keep;
-            q += keep;
+            r = P.r_end;
+            ++s;
+            ++q;
         }
     } else if (threadIdx.x == 32) {  // ---------------- consumer ----------------
         unsigned long long applied = 0, bf = 0, bfc = 0, bs = 0;
@@ -400,79 +339,14 @@ constexpr size_t kRingBytes = kRing * (sizeof(Slot) + 8) + sizeof(ReplayCtl);
 
 }  // namespace
 
-namespace {
-
-// jumps[c - 4][t] = T^(t * c), c in {4, 5}, t in [0, 32): T = xoshiro256's
-// state transition over GF(2)^256 (column-major [256][4] u64 per matrix).
-std::vector<uint64_t> replay_jump_tables() {
-    auto step = [](uint64_t s[4]) {  // RngState::next's state update (rng.hpp:21-31)
-        const uint64_t t = s[1] << 17;
-        s[2] ^= s[0];
-        s[3] ^= s[1];
-        s[1] ^= s[2];
-        s[0] ^= s[3];
-        s[2] ^= t;
-        s[3] = (s[3] << 45) | (s[3] >> 19);
-    };
-    auto matvec = [](const uint64_t* M, const uint64_t in[4], uint64_t out[4]) {
-        out[0] = out[1] = out[2] = out[3] = 0;
-        for (int b = 0; b < 256; ++b)
-            if ((in[b >> 6] >> (b & 63)) & 1)
-                for (int w = 0; w < 4; ++w) out[w] ^= M[b * 4 + w];
-    };
-    auto mul = [&](const std::vector<uint64_t>& A, const std::vector<uint64_t>& B) {  // A * B
-        std::vector<uint64_t> C(256 * 4);
-        for (int b = 0; b < 256; ++b) matvec(A.data(), &B[b * 4], &C[b * 4]);
-        return C;
-    };
-    std::vector<uint64_t> T(256 * 4), I(256 * 4, 0);
-    for (int b = 0; b < 256; ++b) {
-        uint64_t s[4] = {0, 0, 0, 0};
-        s[b >> 6] = 1ULL << (b & 63);
-        I[b * 4 + (b >> 6)] = 1ULL << (b & 63);
-        step(s);
-        for (int w = 0; w < 4; ++w) T[b * 4 + w] = s[w];
-    }
-    std::vector<uint64_t> out;
-    for (int c = 4; c <= 5; ++c) {
-        std::vector<uint64_t> Tc = I;
-        for (int k = 0; k < c; ++k) Tc = mul(T, Tc);
-        std::vector<uint64_t> P = I;
-        for (int t = 0; t < 32; ++t) {
-            out.insert(out.end(), P.begin(), P.end());
-            P = mul(Tc, P);
-        }
-    }
-    return out;
-}
-
-const uint64_t* device_jump_tables(int device) {
-    static std::mutex mu;
-    static std::vector<std::pair<int, uint64_t*>> tabs;
-    std::lock_guard<std::mutex> lock(mu);
-    for (auto& t : tabs)
-        if (t.first == device) return t.second;
-    static const std::vector<uint64_t> host = replay_jump_tables();
-    uint64_t* d = nullptr;
-    PGL_CUDA(cudaMalloc(&d, host.size() * sizeof(uint64_t)));
-    PGL_CUDA(cudaMemcpy(d, host.data(), host.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
-    tabs.emplace_back(device, d);
-    return d;
-}
-
-}  // namespace
-
 void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4, DevStats* stats, const IterArgs& a,
                        void* stream) {
-    int dev = 0;
-    PGL_CUDA(cudaGetDevice(&dev));
-    const uint64_t* jumps = device_jump_tables(dev);
     const size_t cbytes = 32 * g.n_nodes;
     const int use_smem = kRingBytes + cbytes <= kSmemCap ? 1 : 0;
     const size_t bytes = kRingBytes + (use_smem ? cbytes : 0);
     PGL_CUDA(cudaFuncSetAttribute(k_sgd_replay_pc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemCap)));
-    k_sgd_replay_pc<<<1, 64, bytes, static_cast<cudaStream_t>(stream)>>>(g, coords, rng4, stats, a, use_smem, jumps);
+    k_sgd_replay_pc<<<1, 64, bytes, static_cast<cudaStream_t>(stream)>>>(g, coords, rng4, stats, a, use_smem);
     PGL_CUDA(cudaGetLastError());
 }
 
