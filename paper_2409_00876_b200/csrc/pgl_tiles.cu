@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         // Asynchronous pipeline: records and endpoints travel global ->
         // shared by cp.async (no registers held while in flight); the
         // per-unit state between stages lives in shared memory too. With
-        // lookahead L = kAsync, round t
+        // lookahead L = kAsync, round t (= tt - 2L below)
         //   1. waits for the endpoints of unit t and applies its update;
         //   2. waits for the records of unit t+L, resolves its partner (own
         //      copy, or the in-tile owner's slot) and issues its endpoint
@@ -371,11 +371,17 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         auto* s_res = reinterpret_cast<AsyncRes(*)[kWarps][32]>(s_vj + kCS);
         auto* s_fl = reinterpret_cast<uint32_t(*)[kWarps][32]>(s_res + kCS);
         const int wib = static_cast<int>(threadIdx.x >> 5);
-        const int64_t N = static_cast<int64_t>(n_mine);
-        for (int64_t t = -2 * L; t < N; ++t) {
-            if (t >= 0) {  // 1. apply unit t
+        // round tt selects unit tt, resolves unit tt - L, applies unit tt - 2L;
+        // unit x lives in record slot x % kRS and endpoint slot x % kCS, kept
+        // as rotating 32-bit counters (no 64-bit modulo per round)
+        const uint32_t N = static_cast<uint32_t>(n_mine);
+        auto wrap = [](int v, int m) { return v >= m ? v - m : v; };
+        int sel_r = 0;  // tt % kRS
+        int tt_c = 0;   // tt % kCS
+        for (uint32_t tt = 0; tt < N + 2 * L; ++tt) {
+            if (tt >= 2 * L) {  // 1. apply unit tt - 2L
                 cp_async_wait<2 * L - 1>();
-                const int cs = static_cast<int>(t % kCS), rs = static_cast<int>(t % kRS);
+                const int cs = wrap(tt_c + (kCS - (2 * L) % kCS) % kCS, kCS), rs = wrap(sel_r + 1, kRS);
                 const AsyncRes cur = s_res[cs][wib][lane];
                 const bool live = (cur.flags & 1u) && cur.d_ref > 0.0;
                 double vix = 0, viy = 0, vjx = 0, vjy = 0;
@@ -412,11 +418,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     }
                 }
             }
-            const int64_t tr = t + L;  // 2. resolve unit t+L, issue its endpoint copies
-            if (tr >= 0 && tr < N) {
+            if (tt >= L && tt < N + L) {  // 2. resolve unit tt - L, issue its endpoint copies
                 cp_async_wait<2 * L - 2>();
                 __syncwarp();  // in-tile partners read other lanes' copies
-                const int cs = static_cast<int>(tr % kCS), rs = static_cast<int>(tr % kRS);
+                const int cs = wrap(tt_c + (kCS - L % kCS) % kCS, kCS), rs = wrap(sel_r + L + 1, kRS);
                 const uint32_t fs = s_fl[rs][wib][lane];
                 AsyncRes res{0, 0, 0, 0, 0.0};
                 if (fs & 1u) {
@@ -435,10 +440,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 s_res[cs][wib][lane] = res;
             }
             cp_async_commit();
-            const int64_t ts = t + 2 * L;  // 3. select unit t+2L, issue its record copies
-            if (ts < N) {
-                if (ts > 0) advance(u, i0);
-                const int rs = static_cast<int>(ts % kRS);
+            if (tt < N) {  // 3. select unit tt, issue its record copies
+                if (tt > 0) advance(u, i0);
+                const int rs = sel_r;
                 async_ri = s_ri[rs][wib];
                 async_rj = s_rj[rs][wib];
                 const TileSel sel = select(u, i0);
@@ -446,6 +450,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             }
             cp_async_commit();
             __syncwarp();  // slot reuse: every lane is done with this round's shared data
+            sel_r = wrap(sel_r + 1, kRS);
+            tt_c = wrap(tt_c + 1, kCS);
         }
     }
 
