@@ -1,10 +1,11 @@
 """GPU exact path stress (pgl_exact_path_stress) against the reference's
 exact_path_stress (metrics.cpp:75-106) and its C restatement.
 
-Bars: n and skipped identical; mean within 1e-12 relative (the device sums the
-reference's bit-identical per-pair terms in double-double with a fixed fold
-order; the reference sums them serially in double); sigma and CI within 1e-9
-relative; the device result is bit-reproducible run to run."""
+Bars: n and skipped identical; mean within 1e-12 relative (1e-10 at config
+1's 3.7e8 pairs, where the reference's own serial double sum drifts by
+~1e-12; the device sums the reference's bit-identical per-pair terms in
+double-double with a fixed fold order); sigma and CI within 1e-9 relative;
+the device result is bit-reproducible run to run."""
 import numpy as np
 import pytest
 
@@ -77,4 +78,7 @@ def test_exact_stress_config1(pgl, ref, gpu):
     g = pgl.generate_synthetic_pangenome(*C1)
     gr = ref.generate(*C1)
     lay = pgl.run_layout(g, pgl.LayoutConfig(global_seed=101))
-    check(pgl.exact_path_stress(g, lay), ref.exact(gr, lay))
+    # the reference sums 3.7e8 terms serially in double: its own rounding is
+    # ~sqrt(n) * eps ~ 1e-12 relative (measured up to 1.1e-12), so the bar is
+    # 1e-10 here; the device sum is double-double
+    check(pgl.exact_path_stress(g, lay), ref.exact(gr, lay), rtol_mean=1e-10, rtol_sd=1e-9)
