@@ -256,6 +256,13 @@ int pgl_graph_create(int device, const pgl_graph_view* graph, pgl_graph** out);
 int pgl_graph_destroy(pgl_graph* g);
 int pgl_graph_info_get(const pgl_graph* g, pgl_graph_info* out);
 
+/* GFA straight into HBM: the file is parsed on `threads` host threads
+ * (pgl_gfa_parse_file semantics and errors) into node lengths and one 4-byte
+ * word per step; the device builds the step records (build_graph offsets
+ * and path_position by a scan). The 24-byte PathStep arrays are never
+ * materialised on the host. */
+int pgl_graph_create_gfa(int device, const char* path, uint32_t threads, pgl_graph** out);
+
 /* Parity hook: copy the packed device index back to the host, decoded.
  * positions[2*S] = path_position(start), path_position(end) of every step
  * in path order (graph.hpp:98-109); nodes[S] = PathStep::node_id;

@@ -146,6 +146,7 @@ _sig = {
     "pgl_graph_exact_stress": ([_vp, _f64p, C.POINTER(_Report), _f64p], C.c_int),
     "pgl_make_schedule": ([C.POINTER(_View), C.POINTER(_Cfg), _f64p], C.c_int),
     "pgl_gfa_parse_file": ([C.c_char_p, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "pgl_graph_create_gfa": ([C.c_int, C.c_char_p, C.c_uint32, C.POINTER(_vp)], C.c_int),
     "pgl_gfa_parse_buffer": ([C.c_char_p, C.c_uint64, C.c_uint32, C.POINTER(_vp)], C.c_int),
     "pgl_gfa_info_get": ([_vp, C.POINTER(_GfaInfo)], C.c_int),
     "pgl_gfa_view": ([_vp, C.POINTER(_View)], C.c_int),
@@ -617,11 +618,24 @@ class DeviceGraph:
     """A graph packed and resident in HBM (pgl_graph_create): repeated layouts
     and stress evaluations without re-uploading the index."""
 
-    def __init__(self, g: PangenomeGraph, device: int = 0):
+    def __init__(self, g: Optional[PangenomeGraph], device: int = 0, _handle=None):
         self.g, self.device = g, device
-        h = C.c_void_p()
-        _check(_lib.pgl_graph_create(device, C.byref(g.view()), C.byref(h)))
+        if _handle is None:
+            h = C.c_void_p()
+            _check(_lib.pgl_graph_create(device, C.byref(g.view()), C.byref(h)))
+        else:
+            h = _handle
         self.h = h
+        i = self.info()
+        self.n_nodes, self.n_paths, self.total_steps = int(i["n_nodes"]), int(i["n_paths"]), int(i["total_steps"])
+
+    @classmethod
+    def from_gfa(cls, path: str, device: int = 0, threads: int = 0) -> "DeviceGraph":
+        """pgl_graph_create_gfa: parse a GFA on the host into 4-byte step words
+        and build the step records on the device (no PathStep arrays)."""
+        h = C.c_void_p()
+        _check(_lib.pgl_graph_create_gfa(device, os.fsencode(path), threads, C.byref(h)))
+        return cls(None, device, _handle=h)
 
     def close(self):
         if getattr(self, "h", None):
@@ -645,9 +659,9 @@ class DeviceGraph:
                reuse: bool = False, on_iteration=None, stats: Optional[RunStats] = None,
                copy_out: bool = True) -> Optional[np.ndarray]:
         cfg = cfg or LayoutConfig()
-        out = np.zeros(4 * self.g.n_nodes) if copy_out else None
+        out = np.zeros(4 * self.n_nodes) if copy_out else None
         st = _Stats()
-        cb, wants = _callback(on_iteration, self.g.n_nodes)
+        cb, wants = _callback(on_iteration, self.n_nodes)
         e = ext._c() if ext else None
         rc = _lib.pgl_graph_layout(self.h, C.byref(cfg._c()), C.byref(e) if e else None, int(reuse), cb,
                                    wants, None, out.ctypes.data_as(_f64p) if copy_out else None,
@@ -661,7 +675,7 @@ class DeviceGraph:
 
     def export_index(self):
         """(positions [S,2], nodes [S], cum [P+1]) decoded from the device records."""
-        S, P = self.g.total_steps(), self.g.n_paths
+        S, P = self.total_steps, self.n_paths
         pos = np.zeros(2 * S, np.uint64)
         nodes = np.zeros(S, np.uint32)
         cum = np.zeros(P + 1, np.uint64)

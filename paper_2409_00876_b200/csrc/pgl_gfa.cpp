@@ -166,6 +166,9 @@ struct Piece {  // a comma-aligned slice of one P line's step list
 }  // namespace
 
 struct GfaGraph {
+    bool compact = false;                // compact mode: steps as u32 node | reverse << 31 only
+    std::vector<uint32_t> csteps;        // compact: [S] in path order
+    std::vector<uint64_t> path_begin;    // compact: [P+1] cum_steps
     std::vector<uint64_t> node_len;
     std::vector<std::string> path_names;
     std::vector<std::vector<pgl_path_step>> paths;
@@ -175,7 +178,7 @@ struct GfaGraph {
     uint64_t skipped = 0, total_steps = 0;
 };
 
-GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
+GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads, bool compact) {
     // ~4 MiB of text per thread at least: thread start-up costs more than
     // parsing a small file
     const unsigned want = std::max(1u, std::min(threads ? threads : std::thread::hardware_concurrency(), 256u));
@@ -533,20 +536,30 @@ GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
             }
         });
     }
-    G->paths.resize(P);
+    G->compact = compact;
+    G->path_n.assign(P, 0);
     {
         uint64_t acc = 0;
         uint32_t cur = kNone;
         for (auto& pc : pieces) {
             if (pc.path != cur) {
-                if (cur != kNone) G->paths[cur].resize(acc);
+                if (cur != kNone) G->path_n[cur] = acc;
                 cur = pc.path;
                 acc = 0;
             }
             pc.tok0 = acc;
             acc += pc.n_tok;
         }
-        if (cur != kNone) G->paths[cur].resize(acc);
+        if (cur != kNone) G->path_n[cur] = acc;
+    }
+    G->path_begin.assign(P + 1, 0);
+    for (uint32_t p = 0; p < P; ++p) G->path_begin[p + 1] = G->path_begin[p] + G->path_n[p];
+    if (compact) {
+        if (V >= (1ULL << 31)) raise(PGL_ERR_INVALID_PARAMETER, "compact step records need fewer than 2^31 nodes");
+        G->csteps.resize(G->path_begin[P]);
+    } else {
+        G->paths.resize(P);
+        for (uint32_t p = 0; p < P; ++p) G->paths[p].resize(G->path_n[p]);
     }
     {
         std::atomic<uint64_t> nx{0};
@@ -554,7 +567,8 @@ GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
             for (uint64_t k; (k = nx.fetch_add(1)) < pieces.size();) {
                 Piece& pc = pieces[k];
                 const uint64_t ln = plines[pc.path].first;
-                pgl_path_step* out = G->paths[pc.path].data() + pc.tok0;
+                pgl_path_step* out = compact ? nullptr : G->paths[pc.path].data() + pc.tok0;
+                uint32_t* cout = compact ? G->csteps.data() + G->path_begin[pc.path] + pc.tok0 : nullptr;
                 uint64_t i = 0, sum = 0;
                 for_tokens(pc, [&](std::string_view tok) {
                     const uint64_t pos = 2 + pc.tok0 + i;  // after the line-level checks
@@ -575,12 +589,16 @@ GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
                         pc.fail.offer(ln, pos, PGL_ERR_UNKNOWN_SEGMENT, unknown(ln, nm));
                         return false;
                     }
-                    pgl_path_step& s = out[i++];
-                    std::memset(&s, 0, sizeof s);
-                    s.node_id = id;
-                    s.orient = o == '+' ? 0 : 1;
                     const uint64_t len = G->node_len[id];
-                    s.seq_len = static_cast<uint32_t>(len);
+                    if (compact) {
+                        cout[i++] = id | (o == '+' ? 0u : 0x80000000u);
+                    } else {
+                        pgl_path_step& s = out[i++];
+                        std::memset(&s, 0, sizeof s);
+                        s.node_id = id;
+                        s.orient = o == '+' ? 0 : 1;
+                        s.seq_len = static_cast<uint32_t>(len);
+                    }
                     sum += len;
                     return true;
                 });
@@ -608,15 +626,20 @@ GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
         run_threads(T, [&](unsigned) {
             for (uint64_t k; (k = nx.fetch_add(1)) < pieces.size();) {
                 const Piece& pc = pieces[k];
-                pgl_path_step* s = G->paths[pc.path].data() + pc.tok0;
                 uint64_t off = base[k];
                 for (uint64_t i = 0; i < pc.n_tok; ++i) {
-                    s[i].offset = off;
-                    const uint64_t len = G->node_len[s[i].node_id];
+                    uint32_t node;
+                    if (compact) {
+                        node = G->csteps[G->path_begin[pc.path] + pc.tok0 + i] & 0x7FFFFFFFu;
+                    } else {
+                        pgl_path_step& st = G->paths[pc.path][pc.tok0 + i];
+                        st.offset = off;
+                        node = st.node_id;
+                    }
+                    const uint64_t len = G->node_len[node];
                     if (len > std::numeric_limits<uint32_t>::max()) {
                         bfail[k].offer(pc.path, pc.tok0 + i, PGL_ERR_INVALID_PARAMETER,
-                                       "node " + std::to_string(s[i].node_id) +
-                                           " is longer than a step record can hold");
+                                       "node " + std::to_string(node) + " is longer than a step record can hold");
                         break;
                     }
                     off += len;
@@ -629,17 +652,15 @@ GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads) {
     if (b3.line != kNoLine) raise(b3.type, b3.msg);
 
     G->skipped = skipped;
-    G->path_ptrs.resize(P);
-    G->path_n.resize(P);
-    for (uint32_t p = 0; p < P; ++p) {
-        G->path_ptrs[p] = G->paths[p].data();
-        G->path_n[p] = G->paths[p].size();
-        G->total_steps += G->paths[p].size();
+    G->total_steps = G->path_begin[P];
+    if (!compact) {
+        G->path_ptrs.resize(P);
+        for (uint32_t p = 0; p < P; ++p) G->path_ptrs[p] = G->paths[p].data();
     }
     return own.release();
 }
 
-GfaGraph* gfa_parse_file(const char* path, unsigned threads) {
+GfaGraph* gfa_parse_file(const char* path, unsigned threads, bool compact) {
     const int fd = ::open(path, O_RDONLY);
     if (fd < 0) raise(PGL_ERR_INVALID_PARAMETER, std::string("cannot open '") + path + "'");
     struct stat st;
@@ -650,7 +671,7 @@ GfaGraph* gfa_parse_file(const char* path, unsigned threads) {
     const uint64_t size = static_cast<uint64_t>(st.st_size);
     if (size == 0) {
         ::close(fd);
-        return gfa_parse_buffer("", 0, threads);
+        return gfa_parse_buffer("", 0, threads, compact);
     }
     void* m = ::mmap(nullptr, size, PROT_READ, MAP_PRIVATE | MAP_POPULATE, fd, 0);
     ::close(fd);
@@ -661,12 +682,13 @@ GfaGraph* gfa_parse_file(const char* path, unsigned threads) {
         uint64_t n;
         ~Unmap() { ::munmap(p, n); }
     } um{m, size};
-    return gfa_parse_buffer(static_cast<const char*>(m), size, threads);
+    return gfa_parse_buffer(static_cast<const char*>(m), size, threads, compact);
 }
 
 void gfa_free(GfaGraph* g) { delete g; }
 
 void gfa_view(const GfaGraph* g, pgl_graph_view* v) {
+    if (g->compact) raise(PGL_ERR_INVALID_PARAMETER, "a compact GFA parse has no PathStep view");
     std::memset(v, 0, sizeof *v);
     v->n_nodes = g->node_len.size();
     v->node_len = g->node_len.data();
@@ -686,6 +708,17 @@ void gfa_info(const GfaGraph* g, pgl_gfa_info* out) {
 }
 
 const pgl_edge* gfa_edges(const GfaGraph* g) { return g->edges.data(); }
+
+CompactGraph gfa_compact(const GfaGraph* g) {
+    CompactGraph c;
+    c.n_nodes = g->node_len.size();
+    c.node_len = g->node_len.data();
+    c.n_paths = static_cast<uint32_t>(g->path_n.size());
+    c.path_begin = g->path_begin.data();
+    c.path_total = g->path_total.data();
+    c.steps = g->csteps.data();
+    return c;
+}
 const char* gfa_path_name(const GfaGraph* g, uint32_t p) {
     return p < g->path_names.size() ? g->path_names[p].c_str() : nullptr;
 }

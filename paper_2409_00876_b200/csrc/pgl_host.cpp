@@ -454,15 +454,11 @@ namespace {
 // Pack the borrowed reference-format view into 16-byte step records,
 // multithreaded on the host, streamed through two pinned chunks so packing
 // overlaps the H2D copy.
-void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
+// cum_steps, the selection guide and the step-index guide (shared by both
+// ways of building the step records).
+void upload_tables(pgl_graph* G, const std::vector<uint64_t>& cum) {
     const uint64_t S = G->sum.total_steps;
-    const uint32_t P = v->n_paths;
-    std::vector<uint64_t> cum(P + 1, 0);
-    for (uint32_t p = 0; p < P; ++p) cum[p + 1] = cum[p] + v->path_n_steps[p];
-    for (uint32_t p = 0; p < P; ++p)
-        if (v->path_total_len[p] >= (1ULL << 48))
-            raise(PGL_ERR_INVALID_PARAMETER, "path longer than 2^48 nucleotides");
-
+    const uint32_t P = G->n_paths;
     G->step.alloc(S);
     G->cum.alloc(P + 1);
     PGL_CUDA(cudaMemcpyAsync(G->cum.p, cum.data(), (P + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, G->stream));
@@ -498,6 +494,18 @@ void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
     G->guide.alloc(guide.size());
     PGL_CUDA(cudaMemcpyAsync(G->guide.p, guide.data(), guide.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              G->stream));
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
+}
+
+void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
+    const uint64_t S = G->sum.total_steps;
+    const uint32_t P = v->n_paths;
+    std::vector<uint64_t> cum(P + 1, 0);
+    for (uint32_t p = 0; p < P; ++p) cum[p + 1] = cum[p] + v->path_n_steps[p];
+    for (uint32_t p = 0; p < P; ++p)
+        if (v->path_total_len[p] >= (1ULL << 48))
+            raise(PGL_ERR_INVALID_PARAMETER, "path longer than 2^48 nucleotides");
+    upload_tables(G, cum);
 
     const uint64_t kChunk = std::min<uint64_t>(1ULL << 22, std::max<uint64_t>(S, 1));  // <= 4 Mi steps = 64 MiB
     G->pin.alloc(2 * kChunk * sizeof(StepRec));
@@ -552,6 +560,50 @@ pgl_graph* create_graph(int device, const pgl_graph_view* v) {
     G->node_len.assign(v->node_len, v->node_len + v->n_nodes);
     G->path_n_steps.assign(v->path_n_steps, v->path_n_steps + v->n_paths);
     pack_graph(G.get(), v);
+    G->stats.alloc(8);
+    return G.release();
+}
+
+// pgl_graph_create_gfa: GFA -> compact steps on the host -> step records on
+// the device (pgl_pack.cu). The 24-byte PathStep arrays are never built.
+pgl_graph* create_graph_gfa(int device, GfaGraph* gf) {
+    const CompactGraph c = gfa_compact(gf);
+    DeviceGuard dg(device);
+    keep_pool(device);
+    auto G = std::make_unique<pgl_graph>();
+    G->device = device;
+    cudaStream_t st;
+    PGL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    G->set_stream(st);
+    G->n_nodes = c.n_nodes;
+    G->n_paths = c.n_paths;
+    if (c.n_nodes >= (1ULL << 31)) raise(PGL_ERR_INVALID_PARAMETER, "more than 2^31 nodes");
+    G->node_len.assign(c.node_len, c.node_len + c.n_nodes);
+    G->path_n_steps.resize(c.n_paths);
+    ViewSummary sm;
+    for (uint64_t n = 0; n < c.n_nodes; ++n) sm.total_nt += c.node_len[n];
+    for (uint32_t p = 0; p < c.n_paths; ++p) {
+        G->path_n_steps[p] = c.path_begin[p + 1] - c.path_begin[p];
+        sm.max_path_len = std::max(sm.max_path_len, c.path_total[p]);
+        if (G->path_n_steps[p] >= 2) sm.usable = true;
+        if (c.path_total[p] >= (1ULL << 48)) raise(PGL_ERR_INVALID_PARAMETER, "path longer than 2^48 nucleotides");
+    }
+    sm.total_steps = c.path_begin[c.n_paths];
+    G->sum = sm;
+    std::vector<uint64_t> cum(c.path_begin, c.path_begin + c.n_paths + 1);
+    upload_tables(G.get(), cum);
+    // node lengths as u32 (path nodes are checked <= 2^32-1 by the parser)
+    std::vector<uint32_t> len32(c.n_nodes);
+    for (uint64_t n = 0; n < c.n_nodes; ++n)
+        len32[n] = static_cast<uint32_t>(std::min<uint64_t>(c.node_len[n], 0xFFFFFFFFull));
+    DevBuf<uint32_t> dlen, dsteps;
+    dlen.s = dsteps.s = G->stream;
+    dlen.alloc(std::max<uint64_t>(c.n_nodes, 1));
+    dsteps.alloc(std::max<uint64_t>(sm.total_steps, 1));
+    PGL_CUDA(cudaMemcpyAsync(dlen.p, len32.data(), c.n_nodes * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
+    PGL_CUDA(cudaMemcpyAsync(dsteps.p, c.steps, sm.total_steps * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
+    build_records_device(dsteps.p, dlen.p, G->cum.p, c.n_paths, sm.total_steps, G->step.p, G->stream);
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
     G->stats.alloc(8);
     return G.release();
 }
@@ -1269,6 +1321,15 @@ int pgl_exact_path_stress(int device, const pgl_graph_view* v, const double* coo
 struct pgl_gfa {
     pgl::GfaGraph* g;
 };
+
+int pgl_graph_create_gfa(int device, const char* path, uint32_t threads, pgl_graph** out) {
+    return guarded([&] {
+        if (!path || !out) raise(PGL_ERR_INVALID_PARAMETER, "null argument");
+        *out = nullptr;
+        std::unique_ptr<GfaGraph, void (*)(GfaGraph*)> gf(gfa_parse_file(path, threads, /*compact=*/true), gfa_free);
+        *out = create_graph_gfa(device, gf.get());
+    });
+}
 
 int pgl_gfa_parse_file(const char* path, uint32_t threads, pgl_gfa** out) {
     return guarded([&] {

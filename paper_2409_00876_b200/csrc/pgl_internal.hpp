@@ -153,8 +153,19 @@ void run_exact_stress(const DevGraph& g, const double* coords, pgl_stress_report
 
 // GFA ingest (pgl_gfa.cpp).
 struct GfaGraph;
-GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads);
-GfaGraph* gfa_parse_file(const char* path, unsigned threads);
+// compact = true keeps only u32 step words (node | reverse << 31) and
+// cum_steps (the device builds the step records: pgl_graph_create_gfa)
+GfaGraph* gfa_parse_buffer(const char* data, uint64_t size, unsigned threads, bool compact = false);
+GfaGraph* gfa_parse_file(const char* path, unsigned threads, bool compact = false);
+struct CompactGraph {
+    uint64_t n_nodes;
+    const uint64_t* node_len;
+    uint32_t n_paths;
+    const uint64_t* path_begin;  // [P+1]
+    const uint64_t* path_total;  // [P]
+    const uint32_t* steps;       // [S] node | reverse << 31
+};
+CompactGraph gfa_compact(const GfaGraph* g);
 void gfa_free(GfaGraph* g);
 void gfa_view(const GfaGraph* g, pgl_graph_view* v);
 void gfa_info(const GfaGraph* g, pgl_gfa_info* out);
@@ -166,6 +177,10 @@ void layout_write_tsv(const char* path, const double* coords, uint64_t n_nodes, 
 std::string layout_format_tsv(const double* coords, uint64_t n_nodes, uint32_t threads);
 std::vector<double> layout_read_tsv(const char* path, uint32_t threads);
 std::vector<double> layout_read_tsv_buffer(const char* data, uint64_t size, uint32_t threads);
+
+// Step records from compact steps on the device (pgl_pack.cu).
+void build_records_device(const uint32_t* d_steps, const uint32_t* d_node_len, const uint64_t* d_cum, uint32_t P,
+                          uint64_t S, StepRec* d_out, void* stream);
 
 // Small device helpers used by the host driver.
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);

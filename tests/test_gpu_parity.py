@@ -461,3 +461,47 @@ def test_reuse_shuffle_rejected_outside_tiles(pgl, gpu):
     with pytest.raises(pgl.InvalidParameter):
         pgl.run_layout_reuse(g, pgl.LayoutConfig(drf=2, srf=2),
                              ext=pgl.LayoutExt(reuse_shuffle=1, sampling=pgl.SAMPLING_IID))
+
+
+# ---- GFA straight into HBM (pgl_graph_create_gfa) -------------------------------------
+
+def test_graph_from_gfa_matches_reference_index(pgl, ref, gpu, tmp_path):
+    """Device-built step records (compact GFA parse + device offset scan) equal
+    the reference's parse_gfa + build_graph positions bit for bit."""
+    from test_gfa import HAND
+    hand = tmp_path / "hand.gfa"
+    hand.write_text(HAND)
+    for args in [None, (1, 9680, 8, 0.05), (7, 200000, 2, 0.2)]:
+        path = str(hand)
+        if args is not None:
+            path = str(tmp_path / "g.gfa")
+            ref.write_gfa(ref.generate(*args), path)
+        gr, _, _ = ref.parse_gfa_file(path)
+        fo = ref.export(gr)
+        with pgl.DeviceGraph.from_gfa(path) as dg:
+            pos, nodes, cum = dg.export_index()
+            assert (dg.n_nodes, dg.n_paths, dg.total_steps) == (gr.n_nodes, gr.n_paths, gr.total_steps)
+        assert np.array_equal(cum, fo.cum) and np.array_equal(nodes, fo.step_node)
+        assert np.array_equal(pos, fo.positions())
+
+
+def test_graph_from_gfa_lays_out_like_host_path(pgl, ref, gpu, tmp_path):
+    path = str(tmp_path / "c1.gfa")
+    ref.write_gfa(ref.generate(1, 9680, 8, 0.05), path)
+    g = pgl.parse_gfa_file(path)
+    cfg = pgl.LayoutConfig(global_seed=5)
+    with pgl.DeviceGraph.from_gfa(path) as dg:
+        a = dg.layout(cfg, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    b = pgl.run_layout(g, cfg, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    assert np.array_equal(a, b)  # same index, same bit-exact replay
+
+
+def test_graph_from_gfa_errors_match_reference(pgl, ref, gpu, tmp_path):
+    from oracle_ffi import CheckerError
+    path = tmp_path / "bad.gfa"
+    path.write_text("S\ta\tA\nP\tp\ta+,zz-\t*\n")
+    with pytest.raises(CheckerError) as want:
+        ref.parse_gfa_file(str(path))
+    with pytest.raises(pgl.Error) as got:
+        pgl.DeviceGraph.from_gfa(str(path))
+    assert str(got.value) == str(want.value)
