@@ -54,8 +54,10 @@ def main():
     dev_s = None
     try:  # GFA straight into a resident device graph (needs a GPU)
         if P.device_count() > 0:
+            with P.DeviceGraph.from_gfa(path):  # warm: CUDA context, memory pool
+                pass
             t = time.perf_counter()
-            with P.DeviceGraph.from_gfa(path) as dg:
+            with P.DeviceGraph.from_gfa(path):
                 dev_s = time.perf_counter() - t
     except P.Error:
         dev_s = None
