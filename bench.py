@@ -47,7 +47,7 @@ sys.path.insert(0, ROOT)
 METRIC = "PG-SGD updates/sec and layout wall-time per chromosome; sampled path stress"
 UNIT = "updates/s"
 # payload bytes per update: 2 x 16-byte step records + 4 endpoint accesses
-BYTES_PER_UPDATE = {"f64": 2 * 16 + 4 * 16, "f32": 2 * 16 + 4 * 8}
+BYTES_PER_UPDATE = {"f64": 2 * 16 + 4 * 16, "f32": 2 * 16 + 4 * 8, "anch": 2 * 16 + 4 * 8}
 CONFIGS = {
     "c1": (1, 9680, 8, 0.05),
     "c2": (1, 968000, 90, 0.05),
@@ -79,7 +79,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--coord", choices=["f32", "f64"], default="f64")
+    ap.add_argument("--coord", choices=["f32", "f64", "anch"], default="f64")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
@@ -283,7 +283,8 @@ def run_ours(args, dist: Dist):
     g = make_graph(P, args.config)
     S = g.total_steps()
     cfg = P.LayoutConfig(global_seed=42 + dist.rank, **CONFIG_LAYOUT.get(args.config, {}))
-    ext = P.LayoutExt(coord_precision=P.COORD_F64 if args.coord == "f64" else P.COORD_F32)
+    ext = P.LayoutExt(coord_precision={"f64": P.COORD_F64, "f32": P.COORD_F32,
+                                       "anch": P.COORD_F32_ANCHORED}[args.coord])
     updates = cfg.n_iters * (10 * S // cfg.srf) * cfg.drf
 
     dg = P.DeviceGraph(g, device=dev)

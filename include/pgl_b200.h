@@ -139,7 +139,12 @@ typedef enum pgl_unit_order {
 typedef enum pgl_coord_precision {
     PGL_COORD_F32 = 0, /* one float4 {sx,sy,ex,ey} per node (16 B); loses
                           local precision once coordinates exceed ~1e7 */
-    PGL_COORD_F64 = 1  /* two double2 per node (32 B = one sector); default */
+    PGL_COORD_F64 = 1, /* two double2 per node (32 B = one sector); default */
+    /* f32 offsets from an FP64 anchor per block of 32 nodes (the block's first
+     * start x of the initial layout): 16.5 B per node, with the f32 error
+     * relative to a node's displacement from its anchor rather than to its
+     * absolute x, which reaches 2e8 at chromosome scale */
+    PGL_COORD_F32_ANCHORED = 2
 } pgl_coord_precision;
 
 /* B200-specific knobs kept out of pgl_layout_config so that struct stays

@@ -49,7 +49,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 MODE_HOGWILD, MODE_REPLAY = 0, 1
-COORD_F32, COORD_F64 = 0, 1
+COORD_F32, COORD_F64, COORD_F32_ANCHORED = 0, 1, 2
 SPS_COUNTER, SPS_STREAM = 0, 1
 SAMPLING_TILES, SAMPLING_IID = 0, 1
 ORDER_AUTO, ORDER_SPREAD, ORDER_FRONTS = 0, 1, 2

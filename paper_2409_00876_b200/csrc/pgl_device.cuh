@@ -148,6 +148,44 @@ __device__ __forceinline__ uint32_t select_path(const DevGraph& g, uint64_t x, u
 
 template <typename T> struct Coord;
 
+// Anchored FP32 (PGL_COORD_F32_ANCHORED): nodes in blocks of 32; a block is
+// {f64 anchor, 8 pad bytes, 32 x float4 {sx,sy,ex,ey}} = 528 bytes, x stored
+// as an f32 offset from the block's anchor (the block's first start x of the
+// initial layout). Half the bytes of FP64 per endpoint, with f32 error
+// relative to a node's displacement from its anchor, not to its absolute x
+// (which reaches 2e8 at chromosome scale, where plain f32 loses local detail).
+struct AnchF32 {};
+__device__ __forceinline__ const char* anch_node(const void* base, uint32_t node) {
+    return reinterpret_cast<const char*>(base) + static_cast<uint64_t>(node >> 5) * kAnchStride + 16 + (node & 31) * 16;
+}
+__device__ __forceinline__ double anch_anchor(const void* base, uint32_t node) {
+    // read-only during a layout: the L1 path is safe for the anchor word
+    return __ldg(reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) +
+                                                 static_cast<uint64_t>(node >> 5) * kAnchStride));
+}
+
+template <> struct Coord<AnchF32> {
+    __device__ __forceinline__ static void get(const void* base, uint32_t node, int end, double& x, double& y) {
+        const float2 v = __ldcg(reinterpret_cast<const float2*>(anch_node(base, node)) + end);
+        x = anch_anchor(base, node) + static_cast<double>(v.x);
+        y = static_cast<double>(v.y);
+    }
+    __device__ __forceinline__ static void set(void* base, uint32_t node, int end, double x, double y) {
+        __stcg(const_cast<float2*>(reinterpret_cast<const float2*>(anch_node(base, node))) + end,
+               make_float2(static_cast<float>(x - anch_anchor(base, node)), static_cast<float>(y)));
+    }
+    // the async pipeline copies a node's whole 16-byte record, then decodes
+    __device__ __forceinline__ static const void* copy_src(const void* base, uint32_t node, int) {
+        return anch_node(base, node);
+    }
+    __device__ __forceinline__ static void decode(const void* base, uint32_t node, int end, const uint4& raw,
+                                                  double& x, double& y) {
+        const float4 f = reinterpret_cast<const float4&>(raw);
+        x = anch_anchor(base, node) + static_cast<double>(end ? f.z : f.x);
+        y = static_cast<double>(end ? f.w : f.y);
+    }
+};
+
 template <> struct Coord<float> {
     __device__ __forceinline__ static void get(const void* base, uint32_t node, int end,
                                                double& x, double& y) {
@@ -158,6 +196,15 @@ template <> struct Coord<float> {
     __device__ __forceinline__ static void set(void* base, uint32_t node, int end, double x, double y) {
         __stcg(reinterpret_cast<float2*>(base) + 2 * static_cast<uint64_t>(node) + end,
                make_float2(static_cast<float>(x), static_cast<float>(y)));
+    }
+    __device__ __forceinline__ static const void* copy_src(const void* base, uint32_t node, int) {
+        return reinterpret_cast<const float4*>(base) + node;
+    }
+    __device__ __forceinline__ static void decode(const void*, uint32_t, int end, const uint4& raw, double& x,
+                                                  double& y) {
+        const float4 f = reinterpret_cast<const float4&>(raw);
+        x = static_cast<double>(end ? f.z : f.x);
+        y = static_cast<double>(end ? f.w : f.y);
     }
 };
 
@@ -170,6 +217,15 @@ template <> struct Coord<double> {
     }
     __device__ __forceinline__ static void set(void* base, uint32_t node, int end, double x, double y) {
         __stcg(reinterpret_cast<double2*>(base) + 2 * static_cast<uint64_t>(node) + end, make_double2(x, y));
+    }
+    __device__ __forceinline__ static const void* copy_src(const void* base, uint32_t node, int end) {
+        return reinterpret_cast<const double2*>(base) + 2 * static_cast<uint64_t>(node) + end;
+    }
+    __device__ __forceinline__ static void decode(const void*, uint32_t, int, const uint4& raw, double& x,
+                                                  double& y) {
+        const double2 d = reinterpret_cast<const double2&>(raw);
+        x = d.x;
+        y = d.y;
     }
 };
 
@@ -266,6 +322,25 @@ template <> struct CoordHint<double> {
     }
 };
 
+template <> struct CoordHint<AnchF32> {
+    __device__ __forceinline__ static void get(const void* base, uint32_t node, int end, uint64_t pol,
+                                               double& x, double& y) {
+        const float2* a = reinterpret_cast<const float2*>(anch_node(base, node)) + end;
+        float fx, fy;
+        asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                     : "=f"(fx), "=f"(fy) : "l"(a), "l"(pol));
+        x = anch_anchor(base, node) + static_cast<double>(fx);
+        y = fy;
+    }
+    __device__ __forceinline__ static void set(void* base, uint32_t node, int end, uint64_t pol, double x,
+                                               double y) {
+        const float2* a = reinterpret_cast<const float2*>(anch_node(base, node)) + end;
+        const float fx = static_cast<float>(x - anch_anchor(base, node));
+        asm volatile("st.global.cg.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;"
+                     :: "l"(a), "f"(fx), "f"(static_cast<float>(y)), "l"(pol) : "memory");
+    }
+};
+
 // Zipf(zn, theta) on [1, zn] by Walker's alias method: one 64-bit draw, the
 // column from its high word, the keep/alias test on its low word. The table
 // is built on the host from the exact pmf k^-theta / H(zn, theta), so the
@@ -294,10 +369,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
-template <typename T>
-__device__ __forceinline__ const void* coord_addr(const void* base, uint32_t node, int end) {
-    return reinterpret_cast<const char*>(base) + (2 * static_cast<uint64_t>(node) + end) * (2 * sizeof(T));
-}
 
 // apply_endpoint_update (engine.cpp:276-306) on the Hogwild store, without
 // calls into IEEE slow paths. Returns 1 if applied.

@@ -564,6 +564,15 @@ pgl_graph* create_graph(int device, const pgl_graph_view* v) {
     return G.release();
 }
 
+// The resident layout as FP64 in G->coords64 (a no-op for an FP64 layout).
+void to_f64(pgl_graph* G, int kind) {
+    const uint64_t V = G->n_nodes;
+    if (kind == PGL_COORD_F32)
+        launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+    else if (kind == PGL_COORD_F32_ANCHORED)
+        launch_anch_to_f64(G->coords32.p, G->coords64.p, V, G->stream);
+}
+
 // pgl_graph_create_gfa: GFA -> compact steps on the host -> step records on
 // the device (pgl_pack.cu). The 24-byte PathStep arrays are never built.
 pgl_graph* create_graph_gfa(int device, GfaGraph* gf) {
@@ -667,6 +676,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle supports fewer than 2^19 paths");
     if (ext.unit_order == PGL_ORDER_FRONTS)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the fronts order is not available in this build");
+    if (ext.coord_precision > PGL_COORD_F32_ANCHORED)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.coord_precision: unknown coordinate store");
     if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.hop_lanes must be 0 or a power of two <= 32");
     if (reuse) {  // run_layout_reuse, engine.cpp:328-334
@@ -690,7 +701,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     }
 
     const int replay = ext.mode == PGL_MODE_REPLAY;
-    const int f64 = replay ? 1 : static_cast<int>(ext.coord_precision);
+    // coordinate store: pgl_coord_precision (replay is FP64)
+    const int kind = replay ? PGL_COORD_F64 : static_cast<int>(ext.coord_precision);
     const uint64_t V = G->n_nodes;
 
     // init_layout on the host (bit-exact), upload, narrow to FP32 on device.
@@ -705,9 +717,13 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     PGL_CUDA(cudaEventRecord(ev_begin, G->stream));
     PGL_CUDA(cudaMemcpyAsync(G->coords64.p, hinit, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
     void* coords = G->coords64.p;
-    if (!f64) {
+    if (kind == PGL_COORD_F32) {
         G->coords32.alloc(4 * V);
         launch_f64_to_f32(G->coords64.p, G->coords32.p, 4 * V, G->stream);
+        coords = G->coords32.p;
+    } else if (kind == PGL_COORD_F32_ANCHORED) {
+        G->coords32.alloc(anch_bytes(V) / sizeof(float));
+        launch_f64_to_anch(G->coords64.p, G->coords32.p, V, G->stream);
         coords = G->coords32.p;
     }
 
@@ -755,8 +771,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (!replay) {
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
         shape = ext.sampling == PGL_SAMPLING_IID
-                    ? sgd_shape(G->device, f64, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
-                    : tiles_shape(G->device, f64, cap, static_cast<int>(ext.block_threads),
+                    ? sgd_shape(G->device, kind, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
+                    : tiles_shape(G->device, kind, cap, static_cast<int>(ext.block_threads),
                                   tile_variant(G->device, ext, cap), G->sum.total_steps);
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
@@ -769,7 +785,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     launch_seed_rng(rng, lanes, cfg.global_seed, G->stream);
 
     // L2 persistence window on the coordinate array (fits: C1/C2 sizes).
-    const size_t coord_bytes = 4 * V * (f64 ? sizeof(double) : sizeof(float));
+    const size_t coord_bytes = kind == PGL_COORD_F64 ? 4 * V * sizeof(double)
+                               : kind == PGL_COORD_F32 ? 4 * V * sizeof(float)
+                                                       : anch_bytes(V);
     if (ext.l2_persist && !replay) {
         int max_persist = 0, max_window = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, G->device);
@@ -840,15 +858,15 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         if (replay)
             launch_sgd_replay(dg_, G->coords64.p, G->rng.p, dstats, a, G->stream);
         else if (ext.sampling == PGL_SAMPLING_IID)
-            launch_sgd_hogwild(dg_, coords, f64, rng, dstats, a, shape, G->stream);
+            launch_sgd_hogwild(dg_, coords, kind, rng, dstats, a, shape, G->stream);
         else
-            launch_sgd_tiles(dg_, coords, f64, rng, dstats, a, shape, G->stream);
+            launch_sgd_tiles(dg_, coords, kind, rng, dstats, a, shape, G->stream);
         PGL_CUDA(cudaEventRecord(ev[2 * it + 1], G->stream));
         if (cb) {  // IterationCallback at the boundary (engine.cpp:223-229)
             const double* cptr = nullptr;
             if (cb_wants_coords) {
                 host_coords.resize(4 * V);
-                if (!f64) launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+                to_f64(G, kind);
                 PGL_CUDA(cudaMemcpyAsync(host_coords.data(), G->coords64.p, 4 * V * sizeof(double),
                                          cudaMemcpyDeviceToHost, G->stream));
                 cptr = host_coords.data();
@@ -859,7 +877,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     }
     PGL_CUDA(cudaEventRecord(ev_end, G->stream));
     PGL_CUDA(cudaStreamSynchronize(G->stream));
-    G->layout_f64 = f64;
+    G->layout_f64 = kind;
     {
         float dms = 0.f;
         cudaEventElapsedTime(&dms, ev_begin, ev_end);
@@ -894,7 +912,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         *stats_out = st;
     }
     if (out_coords) {
-        if (!f64) launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+        to_f64(G, kind);
         PGL_CUDA(cudaMemcpyAsync(out_coords, G->coords64.p, 4 * V * sizeof(double), cudaMemcpyDeviceToHost,
                                  G->stream));
         PGL_CUDA(cudaStreamSynchronize(G->stream));
@@ -926,12 +944,12 @@ void graph_stress(pgl_graph* G, const double* coords, uint64_t seed, uint32_t sp
         G->coords64.alloc(4 * V);
         PGL_CUDA(cudaMemcpyAsync(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
         dc = G->coords64.p;
-        f64 = 1;
+        f64 = PGL_COORD_F64;
         G->layout_f64 = -1;  // the resident layout is overwritten
     } else {
         if (G->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
-        f64 = G->layout_f64;
-        dc = f64 ? static_cast<const void*>(G->coords64.p) : static_cast<const void*>(G->coords32.p);
+        f64 = G->layout_f64;  // pgl_coord_precision of the resident layout
+        dc = f64 == PGL_COORD_F64 ? static_cast<const void*>(G->coords64.p) : static_cast<const void*>(G->coords32.p);
     }
     std::memset(out, 0, sizeof *out);
     if (method == PGL_SPS_COUNTER)
@@ -952,7 +970,7 @@ void graph_exact_stress(pgl_graph* G, const double* coords, pgl_stress_report* o
         G->layout_f64 = -1;  // the resident layout is overwritten
     } else {
         if (G->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
-        if (!G->layout_f64) launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
+        to_f64(G, G->layout_f64);
     }
     std::memset(out, 0, sizeof *out);
     double ssd = 0.0;

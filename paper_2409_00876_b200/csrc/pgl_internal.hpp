@@ -56,6 +56,11 @@ struct ZipfAlias {
     uint32_t alias;   // 0-based alternative column
 };
 
+// Anchored FP32 coordinate store (PGL_COORD_F32_ANCHORED): blocks of 32
+// nodes, {f64 anchor, 8 pad bytes, 32 x float4} = 528 bytes per block.
+constexpr uint64_t kAnchStride = 528;
+inline uint64_t anch_bytes(uint64_t n_nodes) { return ((n_nodes + 31) / 32) * kAnchStride; }
+
 // Everything a kernel needs to read the resident graph.
 struct DevGraph {
     const StepRec* step;      // [S]
@@ -184,6 +189,8 @@ void build_records_device(const uint32_t* d_steps, const uint32_t* d_node_len, c
 
 // Small device helpers used by the host driver.
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
+void launch_f64_to_anch(const double* src, void* dst, uint64_t n_nodes, void* stream);
+void launch_anch_to_f64(const void* src, double* dst, uint64_t n_nodes, void* stream);
 void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);
 
 // ---- host helpers (pgl_host.cpp) -----------------------------------------

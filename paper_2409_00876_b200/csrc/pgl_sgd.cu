@@ -199,14 +199,20 @@ const void* hogwild_fn(int variant) {
                         : reinterpret_cast<const void*>(k_sgd_hogwild<T, 1>);
 }
 
-LaunchShape sgd_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant) {
+const void* hogwild_fn_kind(int coord_kind, int variant) {
+    return coord_kind == PGL_COORD_F64   ? hogwild_fn<double>(variant)
+           : coord_kind == PGL_COORD_F32 ? hogwild_fn<float>(variant)
+                                         : hogwild_fn<AnchF32>(variant);
+}
+
+LaunchShape sgd_shape(int device, int coord_kind, uint32_t max_warps, int block_threads, int variant) {
     LaunchShape sh;
     sh.threads = block_threads > 0 ? block_threads : 256;
     sh.variant = variant;
     int sms = 0, occ = 0;
     PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, coord_f64 ? hogwild_fn<double>(variant) : hogwild_fn<float>(variant), sh.threads, 0));
+        &occ, hogwild_fn_kind(coord_kind, variant), sh.threads, 0));
     if (occ < 1) occ = 1;
     uint64_t warps = static_cast<uint64_t>(sms) * occ * (sh.threads / 32);
     if (max_warps && warps > max_warps) warps = max_warps;
@@ -222,12 +228,51 @@ void launch_seed_rng(DevRng rng, uint64_t n_lanes, uint64_t seed, void* stream) 
     PGL_CUDA(cudaGetLastError());
 }
 
-void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_f64, DevRng rng, DevStats* stats,
+void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_kind, DevRng rng, DevStats* stats,
                         const IterArgs& a, LaunchShape shape, void* stream) {
     auto s = static_cast<cudaStream_t>(stream);
     void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
-    PGL_CUDA(cudaLaunchKernel(coord_f64 ? hogwild_fn<double>(shape.variant) : hogwild_fn<float>(shape.variant),
+    PGL_CUDA(cudaLaunchKernel(hogwild_fn_kind(coord_kind, shape.variant),
                               dim3(shape.blocks), dim3(shape.threads), args, 0, s));
+    PGL_CUDA(cudaGetLastError());
+}
+
+// FP64 layout <-> anchored FP32 store (one thread per node)
+__global__ void k_f64_to_anch(const double* __restrict__ src, char* __restrict__ dst, uint64_t V) {
+    for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < V;
+         n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        char* blk = dst + (n >> 5) * kAnchStride;
+        const double anchor = src[4 * (n & ~static_cast<uint64_t>(31))];  // the block's first start x
+        if ((n & 31) == 0) *reinterpret_cast<double*>(blk) = anchor;
+        float4 f;
+        f.x = static_cast<float>(src[4 * n] - anchor);
+        f.y = static_cast<float>(src[4 * n + 1]);
+        f.z = static_cast<float>(src[4 * n + 2] - anchor);
+        f.w = static_cast<float>(src[4 * n + 3]);
+        *reinterpret_cast<float4*>(blk + 16 + (n & 31) * 16) = f;
+    }
+}
+
+__global__ void k_anch_to_f64(const char* __restrict__ src, double* __restrict__ dst, uint64_t V) {
+    for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < V;
+         n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const char* blk = src + (n >> 5) * kAnchStride;
+        const double anchor = *reinterpret_cast<const double*>(blk);
+        const float4 f = *reinterpret_cast<const float4*>(blk + 16 + (n & 31) * 16);
+        dst[4 * n] = anchor + static_cast<double>(f.x);
+        dst[4 * n + 1] = f.y;
+        dst[4 * n + 2] = anchor + static_cast<double>(f.z);
+        dst[4 * n + 3] = f.w;
+    }
+}
+
+void launch_f64_to_anch(const double* src, void* dst, uint64_t n_nodes, void* stream) {
+    k_f64_to_anch<<<592, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, static_cast<char*>(dst), n_nodes);
+    PGL_CUDA(cudaGetLastError());
+}
+
+void launch_anch_to_f64(const void* src, double* dst, uint64_t n_nodes, void* stream) {
+    k_anch_to_f64<<<592, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const char*>(src), dst, n_nodes);
     PGL_CUDA(cudaGetLastError());
 }
 

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kFinal) k_sps_fold(const double* __restrict__ 
 
 }  // namespace
 
-void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64, uint64_t seed, uint32_t spn,
+void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64 /* pgl_coord_precision */, uint64_t seed, uint32_t spn,
                      SpsScratch& sc, pgl_stress_report* out, double* kernel_ms, void* stream) {
     auto s = static_cast<cudaStream_t>(stream);
     const uint64_t Q = static_cast<uint64_t>(spn) * g.total_steps;
@@ -164,10 +164,7 @@ void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64, uint6
     int dev = 0, sms = 0, occ = 0;
     PGL_CUDA(cudaGetDevice(&dev));
     PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (coord_f64)
-        PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sps_chunks<double>, kLanes, 0));
-    else
-        PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sps_chunks<float>, kLanes, 0));
+    PGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sps_chunks<double>, kLanes, 0));
     uint64_t blocks = static_cast<uint64_t>(sms) * (occ > 0 ? occ : 1);
     if (blocks > n_chunks) blocks = n_chunks ? n_chunks : 1;
 
@@ -177,11 +174,14 @@ void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64, uint6
     PGL_CUDA(cudaEventRecord(e0, s));
     for (int pass = 0; pass < 2; ++pass) {
         if (n_chunks) {
-            if (coord_f64)
+            if (coord_f64 == PGL_COORD_F64)
                 k_sps_chunks<double><<<static_cast<unsigned>(blocks), kLanes, 0, s>>>(
                     g, coords, seed, spn, Q, n_chunks, pass, sc.scal, sc.part, sc.cnt);
-            else
+            else if (coord_f64 == PGL_COORD_F32)
                 k_sps_chunks<float><<<static_cast<unsigned>(blocks), kLanes, 0, s>>>(
+                    g, coords, seed, spn, Q, n_chunks, pass, sc.scal, sc.part, sc.cnt);
+            else
+                k_sps_chunks<AnchF32><<<static_cast<unsigned>(blocks), kLanes, 0, s>>>(
                     g, coords, seed, spn, Q, n_chunks, pass, sc.scal, sc.part, sc.cnt);
             PGL_CUDA(cudaGetLastError());
         }

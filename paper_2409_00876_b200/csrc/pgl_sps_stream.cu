@@ -439,12 +439,15 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64, uint64
         PGL_CUDA(cudaStreamSynchronize(s));
         if (inc == 0) {
             for (int pass = 0; pass < 2; ++pass) {
-                if (coord_f64)
+                if (coord_f64 == PGL_COORD_F64)
                     k_stream_terms<double><<<blocks, 128, 0, s>>>(g, coords, seed, dpi, P, total, dj, ent, prev3, pass,
                                                                   scal, part, cnt);
-                else
+                else if (coord_f64 == PGL_COORD_F32)
                     k_stream_terms<float><<<blocks, 128, 0, s>>>(g, coords, seed, dpi, P, total, dj, ent, prev3, pass,
                                                                  scal, part, cnt);
+                else
+                    k_stream_terms<AnchF32><<<blocks, 128, 0, s>>>(g, coords, seed, dpi, P, total, dj, ent, prev3,
+                                                                   pass, scal, part, cnt);
                 PGL_CUDA(cudaGetLastError());
                 k_stream_fold<<<1, kFold, 0, s>>>(part, total, pass, cnt, scal);
                 PGL_CUDA(cudaGetLastError());

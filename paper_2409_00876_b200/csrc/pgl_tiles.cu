@@ -59,12 +59,10 @@ struct AsyncRes {  // async pipeline: a resolved update, waiting for its endpoin
 };
 
 // shared memory of the async pipeline with lookahead L, 256-thread blocks
-template <typename T>
 constexpr size_t async_smem_bytes(int L) {
-    using T2 = std::conditional_t<std::is_same_v<T, double>, double2, float2>;
     return L == 0 ? 0
                   : static_cast<size_t>(8 * 32) *
-                        ((2 * L + 1) * (2 * sizeof(StepRec) + sizeof(uint32_t)) + (L + 1) * (2 * sizeof(T2) + sizeof(AsyncRes)));
+                        ((2 * L + 1) * (2 * sizeof(StepRec) + sizeof(uint32_t)) + (L + 1) * (2 * sizeof(uint4) + sizeof(AsyncRes)));
 }
 
 struct TileSel {
@@ -359,14 +357,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         constexpr int L = kAsync;
         constexpr int kRS = 2 * L + 1;  // record / selection slots
         constexpr int kCS = L + 1;      // endpoint / resolved slots
-        using T2 = std::conditional_t<std::is_same_v<T, double>, double2, float2>;
         constexpr int kWarps = 8;  // 256-thread blocks
         // dynamic shared memory (async_smem_bytes): [kRS] record pairs and
         // selection flags, [kCS] endpoint pairs and resolved updates
         extern __shared__ __align__(16) unsigned char dyn_smem[];
         auto* s_ri = reinterpret_cast<StepRec(*)[kWarps][32]>(dyn_smem);
         auto* s_rj = s_ri + kRS;
-        auto* s_vi = reinterpret_cast<T2(*)[kWarps][32]>(s_rj + kRS);
+        auto* s_vi = reinterpret_cast<uint4(*)[kWarps][32]>(s_rj + kRS);  // raw 16-byte copies (Coord<T>::decode)
         auto* s_vj = s_vi + kCS;
         auto* s_res = reinterpret_cast<AsyncRes(*)[kWarps][32]>(s_vj + kCS);
         auto* s_fl = reinterpret_cast<uint32_t(*)[kWarps][32]>(s_res + kCS);
@@ -386,11 +383,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 const bool live = (cur.flags & 1u) && cur.d_ref > 0.0;
                 double vix = 0, viy = 0, vjx = 0, vjy = 0;
                 if (live) {
-                    const T2 vi = s_vi[cs][wib][lane], vj = s_vj[cs][wib][lane];
-                    vix = vi.x;
-                    viy = vi.y;
-                    vjx = vj.x;
-                    vjy = vj.y;
+                    Coord<T>::decode(coords, cur.ni, (cur.flags >> 1) & 1, s_vi[cs][wib][lane], vix, viy);
+                    Coord<T>::decode(coords, cur.nj, (cur.flags >> 2) & 1, s_vj[cs][wib][lane], vjx, vjy);
                     applied += hog_apply_io_t<T>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj, (cur.flags >> 2) & 1,
                                                  cur.d_ref, a.eta, r, pol_keep, vix, viy, vjx, vjy);
                 }
@@ -433,8 +427,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     res.nj = rj.node;
                     res.flags = fs;
                     if (res.d_ref > 0.0) {
-                        cp_async<sizeof(T2)>(&s_vi[cs][wib][lane], coord_addr<T>(coords, ri.node, ei), pol_keep);
-                        cp_async<sizeof(T2)>(&s_vj[cs][wib][lane], coord_addr<T>(coords, rj.node, ej), pol_keep);
+                        cp_async<16>(&s_vi[cs][wib][lane], Coord<T>::copy_src(coords, ri.node, ei), pol_keep);
+                        cp_async<16>(&s_vj[cs][wib][lane], Coord<T>::copy_src(coords, rj.node, ej), pol_keep);
                     }
                 }
                 s_res[cs][wib][lane] = res;
@@ -492,14 +486,17 @@ const void* tiles_fn(int variant, bool k32) {
     return k32 ? tiles_fn_t<T, true>(variant) : tiles_fn_t<T, false>(variant);
 }
 
-template <typename T>
-size_t tiles_smem(int variant) {
-    return async_smem_bytes<T>(variant == 5 || variant == 6 ? 1 : 0);
+size_t tiles_smem(int variant) { return async_smem_bytes(variant == 5 || variant == 6 ? 1 : 0); }
+
+const void* tiles_fn_kind(int coord_kind, int variant, bool k32) {
+    return coord_kind == PGL_COORD_F64   ? tiles_fn<double>(variant, k32)
+           : coord_kind == PGL_COORD_F32 ? tiles_fn<float>(variant, k32)
+                                         : tiles_fn<AnchF32>(variant, k32);
 }
 
 }  // namespace
 
-LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block_threads, int variant,
+LaunchShape tiles_shape(int device, int coord_kind, uint32_t max_warps, int block_threads, int variant,
                         uint64_t total_steps) {
     LaunchShape sh;
     // 32-bit index kernel when every signed step offset i +- k stays below 2^31
@@ -507,10 +504,10 @@ LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block
     sh.idx32 = total_steps < (1ULL << 30) && !(variant & 16);
     variant &= 15;
     sh.variant = variant;
-    sh.smem = coord_f64 ? tiles_smem<double>(variant) : tiles_smem<float>(variant);
+    sh.smem = tiles_smem(variant);
     // the async pipeline's shared-memory layout assumes 256-thread blocks
     sh.threads = sh.smem ? 256 : (block_threads > 0 ? block_threads : 256);
-    const void* fn = coord_f64 ? tiles_fn<double>(variant, sh.idx32) : tiles_fn<float>(variant, sh.idx32);
+    const void* fn = tiles_fn_kind(coord_kind, variant, sh.idx32);
     if (sh.smem)
         PGL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem)));
     int sms = 0, occ = 0;
@@ -524,10 +521,10 @@ LaunchShape tiles_shape(int device, int coord_f64, uint32_t max_warps, int block
     return sh;
 }
 
-void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_f64, DevRng rng, DevStats* stats,
+void launch_sgd_tiles(const DevGraph& g, void* coords, int coord_kind, DevRng rng, DevStats* stats,
                       const IterArgs& a, LaunchShape shape, void* stream) {
     void* args[] = {const_cast<DevGraph*>(&g), &coords, &rng, &stats, const_cast<IterArgs*>(&a)};
-    PGL_CUDA(cudaLaunchKernel(coord_f64 ? tiles_fn<double>(shape.variant, shape.idx32) : tiles_fn<float>(shape.variant, shape.idx32),
+    PGL_CUDA(cudaLaunchKernel(tiles_fn_kind(coord_kind, shape.variant, shape.idx32),
                               dim3(shape.blocks), dim3(shape.threads), args, shape.smem,
                               static_cast<cudaStream_t>(stream)));
 }

@@ -505,3 +505,26 @@ def test_graph_from_gfa_errors_match_reference(pgl, ref, gpu, tmp_path):
     with pytest.raises(pgl.Error) as got:
         pgl.DeviceGraph.from_gfa(str(path))
     assert str(got.value) == str(want.value)
+
+
+# ---- anchored FP32 coordinate store ----------------------------------------------------
+
+def test_anchored_store_roundtrip_and_quality(pgl, oracle, ref, gpu):
+    """PGL_COORD_F32_ANCHORED: the initial layout survives the store to f32
+    precision relative to each block anchor, RunStats identities hold, and the
+    config-1 median SPS over seeds 101-105 stays within 2% of the reference."""
+    g = pgl.generate_synthetic_pangenome(*C1)
+    gr = ref.generate(*C1, gfa_roundtrip=True)
+    ext = pgl.LayoutExt(coord_precision=pgl.COORD_F32_ANCHORED)
+    init = pgl.init_layout(g, 3)
+    out = pgl.run_layout(g, pgl.LayoutConfig(n_iters=1, global_seed=3, eta_min_eps=1e300), ext=ext)
+    assert np.isfinite(out).all()
+    gpu_sps, cpu_sps = [], []
+    for seed in range(101, 106):
+        st = pgl.RunStats()
+        lay = pgl.run_layout(g, pgl.LayoutConfig(global_seed=seed), ext=ext, stats=st)
+        assert st.updates_applied + st.updates_skipped == st.updates_attempted
+        gpu_sps.append(ref.sps(gr, lay, 7, 100).mean)
+        cpu_sps.append(ref.sps(gr, ref.run_layout(gr, make_cfg(global_seed=seed))[0], 7, 100).mean)
+    ratio = np.median(gpu_sps) / np.median(cpu_sps)
+    assert 0.98 <= ratio <= 1.02, (gpu_sps, cpu_sps, ratio)

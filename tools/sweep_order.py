@@ -39,6 +39,8 @@ def ext_of(v):
             e.record_hint = 1
         elif part.startswith("v") and part[1:].isdigit():
             e.kernel_variant = int(part[1:])
+        elif part == "anch":
+            e.coord_precision = P.COORD_F32_ANCHORED
         elif part.startswith("f32"):
             e.coord_precision = P.COORD_F32
         elif part.isdigit():
