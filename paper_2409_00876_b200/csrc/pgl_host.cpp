@@ -689,7 +689,6 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         raise(PGL_ERR_DEGENERATE_GRAPH, "layout needs at least one path with two or more steps");
     if (ext.mode != PGL_MODE_HOGWILD && ext.mode != PGL_MODE_REPLAY) raise(PGL_ERR_INVALID_PARAMETER, "unknown mode");
     if (ext.sampling > PGL_SAMPLING_IID) raise(PGL_ERR_INVALID_PARAMETER, "unknown sampling");
-    if (ext.coord_precision > 1) raise(PGL_ERR_INVALID_PARAMETER, "unknown coord_precision");
 
     DeviceGuard dg(G->device);
     const pgl_graph_view hv = view_of(G);
