@@ -853,6 +853,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : kHopLanes;
             a.reuse_shuffle = ext.reuse_shuffle ? 1 : 0;
         }
+        if (kind == PGL_COORD_F32_ANCHORED && it > 0) launch_reanchor(coords, V, G->stream);
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
         if (replay)
             launch_sgd_replay(dg_, G->coords64.p, G->rng.p, dstats, a, G->stream);

@@ -191,6 +191,7 @@ void build_records_device(const uint32_t* d_steps, const uint32_t* d_node_len, c
 void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
 void launch_f64_to_anch(const double* src, void* dst, uint64_t n_nodes, void* stream);
 void launch_anch_to_f64(const void* src, double* dst, uint64_t n_nodes, void* stream);
+void launch_reanchor(void* store, uint64_t n_nodes, void* stream);
 void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);
 
 // ---- host helpers (pgl_host.cpp) -----------------------------------------

@@ -266,6 +266,36 @@ __global__ void k_anch_to_f64(const char* __restrict__ src, double* __restrict__
     }
 }
 
+// Re-anchor between iterations: a block's anchor moves to its first node's
+// current start x, so the f32 offsets stay small as the layout drifts from
+// the initial one (one warp per block; the anchor update is exact in FP64,
+// each offset is rounded once).
+__global__ void k_reanchor(char* __restrict__ store, uint64_t V) {
+    const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nblocks = (V + 31) / 32;
+    for (uint64_t b = warp; b < nblocks; b += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+        char* blk = store + b * kAnchStride;
+        const double a_old = *reinterpret_cast<const double*>(blk);
+        const float dx0 = *reinterpret_cast<const float*>(blk + 16);  // node 0's start x offset
+        const double a_new = a_old + static_cast<double>(dx0);
+        if (b * 32 + lane < V) {
+            float4* f = reinterpret_cast<float4*>(blk + 16 + lane * 16);
+            float4 v = *f;
+            v.x = static_cast<float>(a_old + static_cast<double>(v.x) - a_new);
+            v.z = static_cast<float>(a_old + static_cast<double>(v.z) - a_new);
+            *f = v;
+        }
+        __syncwarp();
+        if (lane == 0) *reinterpret_cast<double*>(blk) = a_new;
+    }
+}
+
+void launch_reanchor(void* store, uint64_t n_nodes, void* stream) {
+    k_reanchor<<<592, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(store), n_nodes);
+    PGL_CUDA(cudaGetLastError());
+}
+
 void launch_f64_to_anch(const double* src, void* dst, uint64_t n_nodes, void* stream) {
     k_f64_to_anch<<<592, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, static_cast<char*>(dst), n_nodes);
     PGL_CUDA(cudaGetLastError());
