@@ -79,7 +79,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--coord", choices=["f32", "f64", "anch"], default="f64")
+    ap.add_argument("--coord", choices=["auto", "f32", "f64", "anch"], default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
@@ -283,6 +283,8 @@ def run_ours(args, dist: Dist):
     g = make_graph(P, args.config)
     S = g.total_steps()
     cfg = P.LayoutConfig(global_seed=42 + dist.rank, **CONFIG_LAYOUT.get(args.config, {}))
+    if args.coord == "auto":  # the library default: FP64 while it fits L2, anchored FP32 beyond
+        args.coord = "f64" if 32 * g.n_nodes <= (64 << 20) else "anch"
     ext = P.LayoutExt(coord_precision={"f64": P.COORD_F64, "f32": P.COORD_F32,
                                        "anch": P.COORD_F32_ANCHORED}[args.coord])
     updates = cfg.n_iters * (10 * S // cfg.srf) * cfg.drf
@@ -304,7 +306,8 @@ def run_ours(args, dist: Dist):
         tm = dg.timing()
         dev_ms.append(tm.device_ms)
         kern_ms.append(tm.kernel_ms)
-        launches += tm.launches + 1 + (1 if args.coord == "f32" else 0)  # SGD + seed_rng (+ f64->f32)
+        # SGD + seed_rng (+ the f64 -> store conversion, + one re-anchor per iteration after the first)
+        launches += tm.launches + 1 + (0 if args.coord == "f64" else 1) + (cfg.n_iters - 1 if args.coord == "anch" else 0)
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()

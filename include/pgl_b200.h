@@ -144,7 +144,11 @@ typedef enum pgl_coord_precision {
      * start x of the initial layout): 16.5 B per node, with the f32 error
      * relative to a node's displacement from its anchor rather than to its
      * absolute x, which reaches 2e8 at chromosome scale */
-    PGL_COORD_F32_ANCHORED = 2
+    PGL_COORD_F32_ANCHORED = 2,
+    /* default: FP64 while the FP64 array (32 B/node) fits comfortably in L2
+     * (<= 64 MiB), the anchored store beyond (measured at config 3: +15%
+     * updates/s at equal sampled path stress) */
+    PGL_COORD_AUTO = 3
 } pgl_coord_precision;
 
 /* B200-specific knobs kept out of pgl_layout_config so that struct stays
@@ -152,7 +156,7 @@ typedef enum pgl_coord_precision {
 typedef struct pgl_layout_ext {
     uint32_t struct_size;     /* sizeof(pgl_layout_ext) */
     uint32_t mode;            /* pgl_mode */
-    uint32_t coord_precision; /* pgl_coord_precision */
+    uint32_t coord_precision; /* pgl_coord_precision (default PGL_COORD_AUTO) */
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */

@@ -49,7 +49,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 MODE_HOGWILD, MODE_REPLAY = 0, 1
-COORD_F32, COORD_F64, COORD_F32_ANCHORED = 0, 1, 2
+COORD_F32, COORD_F64, COORD_F32_ANCHORED, COORD_AUTO = 0, 1, 2, 3
 SPS_COUNTER, SPS_STREAM = 0, 1
 SAMPLING_TILES, SAMPLING_IID = 0, 1
 ORDER_AUTO, ORDER_SPREAD, ORDER_FRONTS = 0, 1, 2
@@ -251,7 +251,7 @@ class LayoutConfig:
 class LayoutExt:
     """B200 knobs outside LayoutConfig (pgl_layout_ext)."""
     mode: int = MODE_HOGWILD
-    coord_precision: int = COORD_F64
+    coord_precision: int = COORD_AUTO
     max_warps: int = 0
     block_threads: int = 0
     l2_persist: int = 0

@@ -676,7 +676,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle supports fewer than 2^19 paths");
     if (ext.unit_order == PGL_ORDER_FRONTS)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the fronts order is not available in this build");
-    if (ext.coord_precision > PGL_COORD_F32_ANCHORED)
+    if (ext.coord_precision > PGL_COORD_AUTO)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.coord_precision: unknown coordinate store");
     if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.hop_lanes must be 0 or a power of two <= 32");
@@ -701,7 +701,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
 
     const int replay = ext.mode == PGL_MODE_REPLAY;
     // coordinate store: pgl_coord_precision (replay is FP64)
-    const int kind = replay ? PGL_COORD_F64 : static_cast<int>(ext.coord_precision);
+    int kind = replay ? PGL_COORD_F64 : static_cast<int>(ext.coord_precision);
+    if (kind == PGL_COORD_AUTO) kind = 32 * G->n_nodes <= (64ULL << 20) ? PGL_COORD_F64 : PGL_COORD_F32_ANCHORED;
     const uint64_t V = G->n_nodes;
 
     // init_layout on the host (bit-exact), upload, narrow to FP32 on device.
@@ -1208,7 +1209,7 @@ void pgl_layout_ext_default(pgl_layout_ext* e) {
     std::memset(e, 0, sizeof *e);
     e->struct_size = sizeof(pgl_layout_ext);
     e->mode = PGL_MODE_HOGWILD;
-    e->coord_precision = PGL_COORD_F64;
+    e->coord_precision = PGL_COORD_AUTO;
 }
 
 int pgl_graph_create(int device, const pgl_graph_view* v, pgl_graph** out) {
