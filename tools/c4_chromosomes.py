@@ -9,7 +9,7 @@ next graph on the host while the current one is laid out on the device
 with per-chromosome wall times, the makespan and the LPT projection for
 1/2/4/8 GPUs from the measured per-chromosome device times.
 
-usage: python tools/c4_chromosomes.py [--gpus N] [--limit K] [--coord f64|f32]
+usage: python tools/c4_chromosomes.py [--gpus N] [--limit K] [--coord auto|f64|f32|anch]
 """
 import argparse
 import json
@@ -48,13 +48,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=max(1, P.device_count()))
     ap.add_argument("--limit", type=int, default=24)
-    ap.add_argument("--coord", choices=["f32", "f64"], default="f64")
+    ap.add_argument("--coord", choices=["auto", "f32", "f64", "anch"], default="auto")
     ap.add_argument("--sps", action="store_true", help="score every layout on device (spn 10)")
     args = ap.parse_args()
     chroms = list(range(args.limit))
     sizes = [backbone(c) for c in chroms]
     assign, _ = lpt(sizes, args.gpus)
-    ext = P.LayoutExt(coord_precision=P.COORD_F64 if args.coord == "f64" else P.COORD_F32)
+    ext = P.LayoutExt(coord_precision={"auto": P.COORD_AUTO, "f64": P.COORD_F64, "f32": P.COORD_F32,
+                                       "anch": P.COORD_F32_ANCHORED}[args.coord])
     results = {}
     lock = threading.Lock()
 
