@@ -540,3 +540,27 @@ def test_anchored_store_keeps_the_layout_it_was_given(pgl, gpu):
     assert len(seen) == 2 and all(np.isfinite(c).all() for c in seen)
     x = init[0::2]
     assert np.max(np.abs(x)) > 1e5  # absolute x far beyond f32's exact-integer range at this scale
+
+
+# ---- every tile pipeline on awkward shapes ------------------------------------------------
+
+@pytest.mark.parametrize("variant", [1, 2, 5, 6])
+@pytest.mark.parametrize("store", ["f64", "f32", "anch"])
+def test_tile_variants_on_small_and_revisit_graphs(pgl, oracle, gpu, variant, store):
+    """Forced pipelines and coordinate stores on tiny graphs (paths shorter
+    than a unit, one-step paths, reverse steps and revisits), batch sizes
+    1/7/32, drf 2/4 with both reuse semantics: RunStats identities hold and
+    every coordinate stays finite."""
+    prec = {"f64": pgl.COORD_F64, "f32": pgl.COORD_F32, "anch": pgl.COORD_F32_ANCHORED}[store]
+    graphs = [pgl.generate_synthetic_pangenome(*a) for a in SMALL] + [revisit_graph(pgl, oracle)[0]]
+    for g in graphs:
+        for kw, reuse, shuffle in [(dict(batch_size=1), False, 0), (dict(batch_size=7), False, 0),
+                                   (dict(drf=2, srf=2), True, 0), (dict(drf=4, srf=1), True, 1)]:
+            st = pgl.RunStats()
+            cfg = pgl.LayoutConfig(n_iters=4, global_seed=9, **kw)
+            ext = pgl.LayoutExt(kernel_variant=variant, coord_precision=prec, reuse_shuffle=shuffle)
+            fn = pgl.run_layout_reuse if reuse else pgl.run_layout
+            out = fn(g, cfg, stats=st, ext=ext)
+            assert np.isfinite(out).all()
+            assert st.updates_attempted == st.primary_steps * cfg.drf
+            assert st.updates_applied + st.updates_skipped == st.updates_attempted
