@@ -115,33 +115,52 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const uint64_t q0 = static_cast<uint64_t>(unit) * 32;
         const bool active = q0 + lane < a.steps;
         // batch boundaries count this warp's own steps (engine.cpp:115-124)
-        uint32_t in_batch = b0 + lane;
-        if (a.batch >= 32) {
-            if (in_batch >= a.batch) in_batch -= a.batch;
-        } else {
-            in_batch %= a.batch;
-        }
-        bool mine = false;
-        if (active && in_batch == 0) {
-            if (a.force_cooling) {
-                mine = true;
-                ++b_second;
-            } else {
-                mine = r.coin();
-                ++b_first;
-                b_first_cool += mine;
-            }
-        }
-        const int opener = in_batch <= lane ? static_cast<int>(lane - in_batch) : -1;
-        const bool opened = __shfl_sync(kFull, mine, opener < 0 ? 0 : opener);
-        const bool cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
         const uint32_t n_active = static_cast<uint32_t>(a.steps - q0 < 32 ? a.steps - q0 : 32);
-        carry = __shfl_sync(kFull, cooling, n_active - 1);  // batch still open after this unit
-        b0 += n_active;
-        if (a.batch >= 32) {  // b0 < batch and n_active <= 32: one subtraction
-            if (b0 >= a.batch) b0 -= a.batch;
+        bool cooling;
+        if (a.batch == 32 && b0 == 0) {
+            // the default batch size: the unit is exactly one batch, opened by lane 0
+            bool mine = false;
+            if (lane == 0) {
+                if (a.force_cooling) {
+                    mine = true;
+                    ++b_second;
+                } else {
+                    mine = r.coin();
+                    ++b_first;
+                    b_first_cool += mine;
+                }
+            }
+            cooling = a.force_cooling || __shfl_sync(kFull, mine, 0);
+            carry = cooling;
+            b0 = n_active == 32 ? 0 : n_active;
         } else {
-            b0 %= a.batch;
+            uint32_t in_batch = b0 + lane;
+            if (a.batch >= 32) {
+                if (in_batch >= a.batch) in_batch -= a.batch;
+            } else {
+                in_batch %= a.batch;
+            }
+            bool mine = false;
+            if (active && in_batch == 0) {
+                if (a.force_cooling) {
+                    mine = true;
+                    ++b_second;
+                } else {
+                    mine = r.coin();
+                    ++b_first;
+                    b_first_cool += mine;
+                }
+            }
+            const int opener = in_batch <= lane ? static_cast<int>(lane - in_batch) : -1;
+            const bool opened = __shfl_sync(kFull, mine, opener < 0 ? 0 : opener);
+            cooling = a.force_cooling ? true : (opener >= 0 ? opened : carry);
+            carry = __shfl_sync(kFull, cooling, n_active - 1);  // batch still open after this unit
+            b0 += n_active;
+            if (a.batch >= 32) {  // b0 < batch and n_active <= 32: one subtraction
+                if (b0 >= a.batch) b0 -= a.batch;
+            } else {
+                b0 %= a.batch;
+            }
         }
 
         // every lane loads its record, active or not: an in-tile partner of an
