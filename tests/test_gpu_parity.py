@@ -270,14 +270,17 @@ def test_hogwild_converges_and_finite(pgl, oracle, gpu):
 
 
 def test_hogwild_callback_monotone(pgl, oracle, gpu):
-    """test_engine.cpp:335-350: SPS falls along the schedule."""
+    """test_engine.cpp:335-350: SPS falls along the schedule. The reference
+    checks one deterministic threads=1 run with spn 5; a Hogwild run is
+    stochastic, so the estimator here uses spn 40 to keep its own sampling
+    noise well inside the 10% allowance."""
     g, go = both(pgl, oracle, (3, 400, 3, 0.05))
-    sps = [oracle.sps(go, oracle.init_layout(go, 21), 5).mean]
+    sps = [oracle.sps(go, oracle.init_layout(go, 21), 40).mean]
 
     def cb(it, coords, eta, secs):
         assert np.isfinite(coords).all() and secs >= 0.0
         if it in (0, 7, 14, 29):
-            sps.append(oracle.sps(go, coords, 5).mean)
+            sps.append(oracle.sps(go, coords, 40).mean)
 
     pgl.run_layout(g, pgl.LayoutConfig(global_seed=21), on_iteration=cb)
     assert len(sps) == 5
