@@ -410,6 +410,16 @@ int pgl_init_layout(const pgl_graph_view* graph, uint64_t seed, double* out);
  * device, no collective. out_coords[k] receives graph k's layout (may be
  * NULL to skip the copy); seconds[k] the per-graph wall time; assignment[k]
  * the device index used. */
+/* The scheduler's plan alone (host only, no device touched): LPT over the
+ * graphs' update counts (total_steps * n_iters * drf / srf), heaviest first
+ * onto the least-loaded of n_devices, ties to the lowest index.
+ * assignment[k] gets graph k's device index; work[k] (optional) its update
+ * count; device_load[d] (optional) the summed work per device.
+ * pgl_layout_shards runs exactly this plan. */
+int pgl_shard_plan(int n_devices, int n_graphs, const pgl_graph_view* const* graphs,
+                   const pgl_layout_config* cfgs, int* assignment, double* work,
+                   double* device_load);
+
 int pgl_layout_shards(int n_devices, const int* devices, int n_graphs,
                       const pgl_graph_view* const* graphs,
                       const pgl_layout_config* cfgs, const pgl_layout_ext* ext,

@@ -32,7 +32,7 @@ import numpy as np
 __all__ = [
     "LayoutConfig", "LayoutExt", "RunStats", "StressReport", "PangenomeGraph", "DeviceGraph",
     "Timing", "run_layout", "run_layout_reuse", "sampled_path_stress", "make_schedule",
-    "init_layout", "build_graph", "generate_synthetic_pangenome", "layout_shards",
+    "init_layout", "build_graph", "generate_synthetic_pangenome", "layout_shards", "shard_plan",
     "device_count", "Error", "MODE_HOGWILD", "MODE_REPLAY", "COORD_F32", "COORD_F64",
     "SPS_COUNTER", "SPS_STREAM", "SAMPLING_TILES", "SAMPLING_IID", "LIB_PATH",
 ]
@@ -160,6 +160,8 @@ _sig = {
     "pgl_layout_shards": ([C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.POINTER(_View)),
                            C.POINTER(_Cfg), C.POINTER(_Ext), C.POINTER(_f64p), C.POINTER(_Stats),
                            _f64p, C.POINTER(C.c_int)], C.c_int),
+    "pgl_shard_plan": ([C.c_int, C.c_int, C.POINTER(C.POINTER(_View)), C.POINTER(_Cfg),
+                        C.POINTER(C.c_int), _f64p, _f64p], C.c_int),
     "pgl_synthetic_generate": ([C.c_uint64, C.c_uint64, C.c_uint32, C.c_double, C.POINTER(_vp)],
                                C.c_int),
     "pgl_synthetic_view": ([_vp, C.POINTER(_View)], C.c_int),
@@ -709,6 +711,20 @@ class DeviceGraph:
                                            C.byref(r), C.byref(ms)))
         rep = StressReport._of(r)
         return (rep, ms.value) if return_ms else rep
+
+
+def shard_plan(graphs: Sequence[PangenomeGraph], cfgs: Sequence[LayoutConfig], n_devices: int):
+    """The plan layout_shards runs (pgl_shard_plan), computed on the host:
+    returns (assignment, work, device_load) with work = updates per graph."""
+    n = len(graphs)
+    views = (C.POINTER(_View) * max(n, 1))(*[C.pointer(g.view()) for g in graphs])
+    cs = (_Cfg * max(n, 1))(*[c._c() for c in cfgs])
+    assign = (C.c_int * max(n, 1))()
+    work = np.zeros(max(n, 1))
+    load = np.zeros(max(n_devices, 1))
+    _check(_lib.pgl_shard_plan(n_devices, n, views, cs, assign, work.ctypes.data_as(_f64p),
+                               load.ctypes.data_as(_f64p)))
+    return list(assign)[:n], work[:n], load[:n_devices]
 
 
 def layout_shards(graphs: Sequence[PangenomeGraph], cfgs: Sequence[LayoutConfig], devices: Sequence[int],

@@ -1504,29 +1504,46 @@ int pgl_synthetic_free(pgl_synthetic* s) {
     return PGL_OK;
 }
 
+int pgl_shard_plan(int n_devices, int n_graphs, const pgl_graph_view* const* graphs,
+                   const pgl_layout_config* cfgs, int* assignment, double* work, double* device_load) {
+    return guarded([&] {
+        if (n_devices < 1) raise(PGL_ERR_INVALID_PARAMETER, "need at least one device");
+        if (n_graphs < 0 || (n_graphs && (!graphs || !cfgs || !assignment)))
+            raise(PGL_ERR_INVALID_PARAMETER, "null graph list");
+        // LPT: heaviest graph first onto the least-loaded device;
+        // a graph's work is its update count, total_steps * n_iters * drf / srf.
+        std::vector<double> w(n_graphs);
+        for (int k = 0; k < n_graphs; ++k) {
+            const ViewSummary s = summarize(graphs[k]);
+            validate_config(cfgs[k]);
+            w[k] = static_cast<double>(s.total_steps) * cfgs[k].n_iters * cfgs[k].drf / cfgs[k].srf;
+            if (work) work[k] = w[k];
+        }
+        std::vector<int> order(n_graphs);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return w[a] > w[b]; });
+        std::vector<double> load(n_devices, 0.0);
+        for (int k : order) {
+            const int d = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+            load[d] += w[k];
+            assignment[k] = d;
+        }
+        if (device_load) std::copy(load.begin(), load.end(), device_load);
+    });
+}
+
 int pgl_layout_shards(int n_devices, const int* devices, int n_graphs, const pgl_graph_view* const* graphs,
                       const pgl_layout_config* cfgs, const pgl_layout_ext* ext, double* const* out_coords,
                       pgl_run_stats* stats, double* seconds, int* assignment) {
     return guarded([&] {
         if (n_devices < 1 || !devices) raise(PGL_ERR_INVALID_PARAMETER, "need at least one device");
-        if (n_graphs < 0 || (n_graphs && (!graphs || !cfgs))) raise(PGL_ERR_INVALID_PARAMETER, "null graph list");
-        // LPT: heaviest graph first onto the least-loaded device.
-        std::vector<double> work(n_graphs);
-        for (int k = 0; k < n_graphs; ++k) {
-            const ViewSummary s = summarize(graphs[k]);
-            validate_config(cfgs[k]);
-            work[k] = static_cast<double>(s.total_steps) * cfgs[k].n_iters * cfgs[k].drf / cfgs[k].srf;
-        }
-        std::vector<int> order(n_graphs);
-        std::iota(order.begin(), order.end(), 0);
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return work[a] > work[b]; });
-        std::vector<double> load(n_devices, 0.0);
+        std::vector<int> plan(std::max(n_graphs, 1));
+        const int rc = pgl_shard_plan(n_devices, n_graphs, graphs, cfgs, plan.data(), nullptr, nullptr);
+        if (rc != PGL_OK) throw Failure(rc, pgl_last_error());
         std::vector<std::vector<int>> queue(n_devices);
-        for (int k : order) {
-            const int d = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-            load[d] += work[k];
-            queue[d].push_back(k);
-            if (assignment) assignment[k] = d;
+        for (int k = 0; k < n_graphs; ++k) {
+            queue[plan[k]].push_back(k);
+            if (assignment) assignment[k] = plan[k];
         }
         std::vector<std::thread> pool;
         std::vector<std::string> errs(n_devices);
