@@ -199,14 +199,17 @@ def hbm_peak():
 
 
 def ncu_traffic(config: str, coord: str):
-    """dram bytes per SGD launch from the committed ncu --set full capture."""
+    """(dram bytes per SGD launch, cache/sector summary) from the committed
+    ncu --set full capture (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d[f"{config}_{coord}"]["dram_bytes_per_launch"]
+            e = json.load(f)[f"{config}_{coord}"]
     except (OSError, KeyError, ValueError):
-        return None
+        return None, None
+    keys = ("l2_hit_pct", "l1_hit_pct", "ld_bytes_per_sector", "st_bytes_per_sector", "lsu_sectors_per_update",
+            "source")
+    return e.get("dram_bytes_per_launch"), {k: e[k] for k in keys if k in e}
 
 
 # ---- CPU baseline: the reference itself --------------------------------------------
@@ -346,7 +349,7 @@ def run_ours(args, dist: Dist):
     peak, peak_src = hbm_peak()
     bytes_per_launch = (10 * S // cfg.srf) * cfg.drf * BYTES_PER_UPDATE[args.coord]
     achieved = bytes_per_launch / (sgd_launch_ms / 1e3) / 1e9
-    traffic = ncu_traffic(args.config, args.coord)
+    traffic, ncu_cache = ncu_traffic(args.config, args.coord)
     if dist.rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -368,7 +371,7 @@ def run_ours(args, dist: Dist):
                          "bytes_per_update": BYTES_PER_UPDATE[args.coord],
                          "bytes_model": "payload: 2 step records + 2 endpoint reads + 2 endpoint writes",
                          "launch_ms": sgd_launch_ms,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src, "ncu": ncu_cache},
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clk,

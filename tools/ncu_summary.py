@@ -43,6 +43,14 @@ for r in data:
         "dram_GBps": (rd + wr) / (ms / 1e3) / 1e9,
         "updates_per_s": upd / (ms / 1e3),
         "l2_hit_pct": val(r, "lts__t_sector_hit_rate.pct"),
+        "l1_hit_pct": val(r, "l1tex__t_sector_hit_rate.pct"),
+        # sector efficiency: useful bytes per 32-byte sector the LSU requested
+        "ld_bytes_per_sector": val(r, "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio"),
+        "st_bytes_per_sector": val(r, "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio"),
+        "ldgsts_sectors_per_update": (val(r, "sm__sass_l1tex_t_sectors_pipe_lsu_mem_global_op_ldgsts_cache_bypass.sum")
+                                      or 0) / upd,
+        "ld_sectors_per_update": (val(r, "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum") or 0) / upd,
+        "st_sectors_per_update": (val(r, "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum") or 0) / upd,
         "l2_throughput_pct": val(r, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
         "dram_throughput_pct": val(r, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
         "sm_throughput_pct": val(r, "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
