@@ -567,3 +567,53 @@ def test_tile_variants_on_small_and_revisit_graphs(pgl, oracle, gpu, variant, st
             assert np.isfinite(out).all()
             assert st.updates_attempted == st.primary_steps * cfg.drf
             assert st.updates_applied + st.updates_skipped == st.updates_attempted
+
+
+# ---- positions beyond 32 bits (graph.hpp:98-109 with u64 offsets) ---------------
+
+def long_node_graph(pgl, oracle):
+    """Nodes up to 2^32 - 1 nt (the longest a step record holds,
+    graph.cpp:45-47): path positions reach ~1.3e10, so the packed records'
+    48-bit positions and the FP64 coordinates both leave the 32-bit range."""
+    lens = [2**32 - 1, 7, 2**31, 5, 3_000_000_000, 9, 2**32 - 2]
+    walks = [[(0, 0), (1, 1), (2, 0), (3, 0), (4, 1), (5, 0), (6, 0)],
+             [(6, 1), (4, 0), (1, 0), (0, 1), (2, 1), (2, 1), (5, 1)],
+             [(3, 0), (0, 0), (6, 0)]]
+    return pgl.build_graph(lens, walks), oracle.build(lens, walks), lens, walks
+
+
+def test_long_nodes_index_bit_exact(pgl, oracle, gpu):
+    g, go, _, _ = long_node_graph(pgl, oracle)
+    fo = oracle.export(go)
+    assert int(fo.positions().max()) > 2**33
+    with pgl.DeviceGraph(g) as dg:
+        pos, nodes, cum = dg.export_index()
+    assert np.array_equal(pos, fo.positions())
+    assert np.array_equal(nodes, fo.step_node)
+    assert np.array_equal(cum, fo.cum)
+
+
+def test_long_nodes_replay_sps_and_exact(pgl, oracle, ref, gpu):
+    g, go, lens, walks = long_node_graph(pgl, oracle)
+    cfg, ocfg = cfg_pair(pgl, n_iters=5, global_seed=31, batch_size=4)
+    st = pgl.RunStats()
+    out = pgl.run_layout(g, cfg, stats=st, ext=pgl.LayoutExt(mode=pgl.MODE_REPLAY))
+    want, rst = oracle.run_layout(go, ocfg)
+    assert stats_tuple(st) == stats_tuple(rst)
+    assert np.array_equal(out, want)
+    # sampled stress: bit-exact with the C restatement of the counter estimator
+    got = pgl.sampled_path_stress(g, out, 7, 50)
+    assert stress_tuple(got) == stress_tuple(oracle.sps_counter(go, out, 7, 50))
+    # exact stress against the reference's own metric
+    e, w = pgl.exact_path_stress(g, out), ref.exact(ref.build(lens, walks), out)
+    assert (e.n, e.skipped) == (w.n, w.skipped)
+    assert e.mean == pytest.approx(w.mean, rel=1e-12)
+
+
+def test_long_nodes_hogwild_converges(pgl, oracle, gpu):
+    g, go, _, _ = long_node_graph(pgl, oracle)
+    init = oracle.sps(go, oracle.init_layout(go, 3), 20).mean
+    for variant in (0, 1, 6):
+        out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=3), ext=pgl.LayoutExt(kernel_variant=variant))
+        assert np.isfinite(out).all()
+        assert oracle.sps(go, out, 20).mean < init
