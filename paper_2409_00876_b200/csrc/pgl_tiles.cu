@@ -106,12 +106,20 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     // Stage A: batch decision, i's record (coalesced), partner selection.
     StepRec* async_ri = nullptr;  // kAsync: shared-memory destinations of select's record copies
     StepRec* async_rj = nullptr;
+    // Unit coins: every fair bit a lane needs for one unit -- the batch coin
+    // (bit 0, batch openers), the group's hop sign (bit 1, hop leaders; a
+    // lane's own sign when it draws its own hop), the two endpoint coins
+    // (bits 2-3) -- comes from the top 4 bits of one xoshiro256+ output per
+    // unit instead of a fresh output per coin (the reference's flip_coin
+    // takes one output's top bit, rng.hpp:40): the same i.i.d. fair coins at
+    // a third to a quarter of the generator work.
     auto select = [&](UX unit, UX unit_i0) -> TileSel {
         TileSel o;
         o.flags = 0;
         o.src = 0;
         o.path = 0;
         o.ri = o.rj = StepRec{0, 0, 0, 0};
+        const uint32_t coins = static_cast<uint32_t>(r.next() >> 60);
         const uint64_t q0 = static_cast<uint64_t>(unit) * 32;
         const bool active = q0 + lane < a.steps;
         // batch boundaries count this warp's own steps (engine.cpp:115-124)
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     mine = true;
                     ++b_second;
                 } else {
-                    mine = r.coin();
+                    mine = coins & 1u;
                     ++b_first;
                     b_first_cool += mine;
                 }
@@ -146,7 +154,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     mine = true;
                     ++b_second;
                 } else {
-                    mine = r.coin();
+                    mine = coins & 1u;
                     ++b_first;
                     b_first_cool += mine;
                 }
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             if (active && n >= 2 && (win_lead || hop_lead)) {
                 draw = r.next();
                 tag |= (1u << 30) | (cooling ? (1u << 29) : 0u);
-                if (cooling) tag |= static_cast<uint32_t>(r.next() >> 63) << 31;
+                if (cooling) tag |= ((coins >> 1) & 1u) << 31;
             }
         }
         const int lead = cooling ? static_cast<int>(lane & ~(a.hop_lanes - 1)) : 0;
@@ -211,13 +219,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         if (!active || n < 2) return o;
         const SX i = static_cast<SX>(gi - pbase);
         SX j;
-        uint64_t bits;
         if (cooling) {
             const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
             const uint64_t zt = __ldg(&g.pc[p].ztab);
             const SX k = static_cast<SX>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
-            bits = r.next();
-            const SX sign = (shared ? (tag >> 31) : ((bits >> 61) & 1)) ? 1 : -1;
+            const SX sign = (shared ? (tag >> 31) : ((coins >> 1) & 1u)) ? 1 : -1;
             j = i + sign * k;
             if (j < 0 || j >= n) {
                 j = i - sign * k;
@@ -240,10 +246,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 j = static_cast<SX>(r.below(static_cast<uint64_t>(n)));
                 if (j == i) return o;
             }
-            bits = r.next();
         }
         const UX gj = pbase + static_cast<UX>(j);
-        uint32_t fl = 1u | ((bits >> 63) ? 0u : 2u) | (((bits >> 62) & 1) ? 0u : 4u);
+        // coin true -> start (coin_endpoint, engine.cpp:89-91): flag set = end
+        uint32_t fl = 1u | ((coins & 4u) ? 0u : 2u) | ((coins & 8u) ? 0u : 4u);
         if (gj >= i0 && gj - i0 < 32) {
             fl |= 8u;
             o.src = static_cast<uint32_t>(gj - i0);
