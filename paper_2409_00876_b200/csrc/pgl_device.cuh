@@ -158,6 +158,10 @@ struct AnchF32 {};
 __device__ __forceinline__ const char* anch_node(const void* base, uint32_t node) {
     return reinterpret_cast<const char*>(base) + static_cast<uint64_t>(node >> 5) * kAnchStride + 16 + (node & 31) * 16;
 }
+__device__ __forceinline__ const double* anch_anchor_ptr(const void* base, uint32_t node) {
+    return reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) +
+                                           static_cast<uint64_t>(node >> 5) * kAnchStride);
+}
 __device__ __forceinline__ double anch_anchor(const void* base, uint32_t node) {
     // read-only during a layout: the L1 path is safe for the anchor word
     return __ldg(reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) +
@@ -182,6 +186,14 @@ template <> struct Coord<AnchF32> {
                                                   double& x, double& y) {
         const float4 f = reinterpret_cast<const float4&>(raw);
         x = anch_anchor(base, node) + static_cast<double>(end ? f.z : f.x);
+        y = static_cast<double>(end ? f.w : f.y);
+    }
+    // the same with the block anchor already at hand (the async pipeline
+    // copies it to shared memory beside the node record)
+    __device__ __forceinline__ static void decode_anchored(int end, const uint4& raw, double anchor, double& x,
+                                                           double& y) {
+        const float4 f = reinterpret_cast<const float4&>(raw);
+        x = anchor + static_cast<double>(end ? f.z : f.x);
         y = static_cast<double>(end ? f.w : f.y);
     }
 };
@@ -334,8 +346,12 @@ template <> struct CoordHint<AnchF32> {
     }
     __device__ __forceinline__ static void set(void* base, uint32_t node, int end, uint64_t pol, double x,
                                                double y) {
+        set_anchored(base, node, end, pol, x, y, anch_anchor(base, node));
+    }
+    __device__ __forceinline__ static void set_anchored(void* base, uint32_t node, int end, uint64_t pol, double x,
+                                                        double y, double anchor) {
         const float2* a = reinterpret_cast<const float2*>(anch_node(base, node)) + end;
-        const float fx = static_cast<float>(x - anch_anchor(base, node));
+        const float fx = static_cast<float>(x - anchor);
         asm volatile("st.global.cg.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;"
                      :: "l"(a), "f"(fx), "f"(static_cast<float>(y)), "l"(pol) : "memory");
     }
@@ -389,10 +405,11 @@ __device__ __forceinline__ uint32_t hog_update_t(void* coords, uint32_t ni, int 
 
 // hog_apply_t that also returns the new v_i (warp-shuffle reuse keeps
 // updating the same i endpoint).
-template <typename T>
+template <typename T, bool kGivenAnchors = false>
 __device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
                                                  double d_ref, double eta, Xo& r, uint64_t pol, double& vix,
-                                                 double& viy, double vjx, double vjy);
+                                                 double& viy, double vjx, double vjy, double anc_i = 0.0,
+                                                 double anc_j = 0.0);
 
 // The arithmetic and write-back half of hog_update_t, on endpoint values the
 // caller loaded (d_ref > 0).
@@ -403,10 +420,13 @@ __device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int e
     return hog_apply_io_t<T>(coords, ni, ei, nj, ej, d_ref, eta, r, pol, vix, viy, vjx, vjy);
 }
 
-template <typename T>
+// kGivenAnchors (anchored store only): the caller holds both nodes' block
+// anchors, so the write-back does not re-read them.
+template <typename T, bool kGivenAnchors>
 __device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
                                                  double d_ref, double eta, Xo& r, uint64_t pol, double& vix,
-                                                 double& viy, double vjx, double vjy) {
+                                                 double& viy, double vjx, double vjy, double anc_i,
+                                                 double anc_j) {
     double mu = eta * rcp_nr(d_ref * d_ref);
     if (mu > 1.0) mu = 1.0;
     const double dx = vix - vjx;
@@ -428,8 +448,13 @@ __device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, in
     const double delta = mu * (mag - d_ref) * 0.5;
     vix -= delta * ux;
     viy -= delta * uy;
-    CoordHint<T>::set(coords, ni, ei, pol, vix, viy);
-    CoordHint<T>::set(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy);
+    if constexpr (kGivenAnchors) {
+        CoordHint<T>::set_anchored(coords, ni, ei, pol, vix, viy, anc_i);
+        CoordHint<T>::set_anchored(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy, anc_j);
+    } else {
+        CoordHint<T>::set(coords, ni, ei, pol, vix, viy);
+        CoordHint<T>::set(coords, nj, ej, pol, vjx + delta * ux, vjy + delta * uy);
+    }
     return 1;
 }
 

@@ -58,11 +58,13 @@ struct AsyncRes {  // async pipeline: a resolved update, waiting for its endpoin
     double d_ref;
 };
 
-// shared memory of the async pipeline with lookahead L, 256-thread blocks
-constexpr size_t async_smem_bytes(int L) {
+// shared memory of the async pipeline with lookahead L, 256-thread blocks;
+// the anchored store adds the two endpoints' block anchors per update
+constexpr size_t async_smem_bytes(int L, bool anchored) {
     return L == 0 ? 0
                   : static_cast<size_t>(8 * 32) *
-                        ((2 * L + 1) * (2 * sizeof(StepRec) + sizeof(uint32_t)) + (L + 1) * (2 * sizeof(uint4) + sizeof(AsyncRes)));
+                        ((2 * L + 1) * (2 * sizeof(StepRec) + sizeof(uint32_t)) +
+                         (L + 1) * (2 * sizeof(uint4) + sizeof(AsyncRes) + (anchored ? 2 * sizeof(double) : 0)));
 }
 
 struct TileSel {
@@ -392,6 +394,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         auto* s_vj = s_vi + kCS;
         auto* s_res = reinterpret_cast<AsyncRes(*)[kWarps][32]>(s_vj + kCS);
         auto* s_fl = reinterpret_cast<uint32_t(*)[kWarps][32]>(s_res + kCS);
+        // anchored store: block anchors of i and j, copied beside the records
+        constexpr bool kAnch = std::is_same_v<T, AnchF32>;
+        auto* s_ai = reinterpret_cast<double(*)[kWarps][32]>(s_fl + kRS);
+        auto* s_aj = s_ai + kCS;
         const int wib = static_cast<int>(threadIdx.x >> 5);
         // round tt selects unit tt, resolves unit tt - L, applies unit tt - 2L;
         // unit x lives in record slot x % kRS and endpoint slot x % kCS, kept
@@ -408,10 +414,20 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 const bool live = (cur.flags & 1u) && cur.d_ref > 0.0;
                 double vix = 0, viy = 0, vjx = 0, vjy = 0;
                 if (live) {
-                    Coord<T>::decode(coords, cur.ni, (cur.flags >> 1) & 1, s_vi[cs][wib][lane], vix, viy);
-                    Coord<T>::decode(coords, cur.nj, (cur.flags >> 2) & 1, s_vj[cs][wib][lane], vjx, vjy);
-                    applied += hog_apply_io_t<T>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj, (cur.flags >> 2) & 1,
-                                                 cur.d_ref, a.eta, r, pol_keep, vix, viy, vjx, vjy);
+                    if constexpr (kAnch) {
+                        const double ai = s_ai[cs][wib][lane], aj = s_aj[cs][wib][lane];
+                        Coord<T>::decode_anchored((cur.flags >> 1) & 1, s_vi[cs][wib][lane], ai, vix, viy);
+                        Coord<T>::decode_anchored((cur.flags >> 2) & 1, s_vj[cs][wib][lane], aj, vjx, vjy);
+                        applied += hog_apply_io_t<T, true>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj,
+                                                           (cur.flags >> 2) & 1, cur.d_ref, a.eta, r, pol_keep, vix,
+                                                           viy, vjx, vjy, ai, aj);
+                    } else {
+                        Coord<T>::decode(coords, cur.ni, (cur.flags >> 1) & 1, s_vi[cs][wib][lane], vix, viy);
+                        Coord<T>::decode(coords, cur.nj, (cur.flags >> 2) & 1, s_vj[cs][wib][lane], vjx, vjy);
+                        applied += hog_apply_io_t<T>(coords, cur.ni, (cur.flags >> 1) & 1, cur.nj,
+                                                     (cur.flags >> 2) & 1, cur.d_ref, a.eta, r, pol_keep, vix, viy,
+                                                     vjx, vjy);
+                    }
                 }
                 if (a.drf > 1) {
                     const StepRec ri = s_ri[rs][wib][lane];
@@ -454,6 +470,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     if (res.d_ref > 0.0) {
                         cp_async<16>(&s_vi[cs][wib][lane], Coord<T>::copy_src(coords, ri.node, ei), pol_keep);
                         cp_async<16>(&s_vj[cs][wib][lane], Coord<T>::copy_src(coords, rj.node, ej), pol_keep);
+                        if constexpr (kAnch) {
+                            cp_async<8>(&s_ai[cs][wib][lane], anch_anchor_ptr(coords, ri.node), pol_keep);
+                            cp_async<8>(&s_aj[cs][wib][lane], anch_anchor_ptr(coords, rj.node), pol_keep);
+                        }
                     }
                 }
                 s_res[cs][wib][lane] = res;
@@ -511,7 +531,9 @@ const void* tiles_fn(int variant, bool k32) {
     return k32 ? tiles_fn_t<T, true>(variant) : tiles_fn_t<T, false>(variant);
 }
 
-size_t tiles_smem(int variant) { return async_smem_bytes(variant == 5 || variant == 6 ? 1 : 0); }
+size_t tiles_smem(int variant, int coord_kind) {
+    return async_smem_bytes(variant == 5 || variant == 6 ? 1 : 0, coord_kind == PGL_COORD_F32_ANCHORED);
+}
 
 const void* tiles_fn_kind(int coord_kind, int variant, bool k32) {
     return coord_kind == PGL_COORD_F64   ? tiles_fn<double>(variant, k32)
@@ -529,7 +551,7 @@ LaunchShape tiles_shape(int device, int coord_kind, uint32_t max_warps, int bloc
     sh.idx32 = total_steps < (1ULL << 30) && !(variant & 16);
     variant &= 15;
     sh.variant = variant;
-    sh.smem = tiles_smem(variant);
+    sh.smem = tiles_smem(variant, coord_kind);
     // the async pipeline's shared-memory layout assumes 256-thread blocks
     sh.threads = sh.smem ? 256 : (block_threads > 0 ? block_threads : 256);
     const void* fn = tiles_fn_kind(coord_kind, variant, sh.idx32);
