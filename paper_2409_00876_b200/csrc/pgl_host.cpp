@@ -477,7 +477,12 @@ void upload_tables(pgl_graph* G, const std::vector<uint64_t>& cum) {
     {   // step-index guide: path containing step b << shift (path_of_step)
         uint32_t L = 1;
         while ((1ULL << L) < std::max<uint64_t>(S, 2)) ++L;
-        const uint32_t sb = std::min<uint32_t>(L, 14);
+        // ~16 buckets per path keeps the forward scan at ~1 step while the
+        // table stays small enough to live in L1 next to the async
+        // pipeline's shared memory (2^10 entries = 4 KB at 90 paths)
+        uint32_t want = 10;
+        while ((1u << want) < 16u * std::max<uint32_t>(P, 1) && want < 14) ++want;
+        const uint32_t sb = std::min<uint32_t>(L, want);
         G->sguide_bits = sb;
         G->sguide_shift = L - sb;
         std::vector<uint32_t> sg(1u << sb, 0);

@@ -43,11 +43,32 @@ __device__ __forceinline__ void flush_stat(DevStats* st, int idx, uint32_t v) {
     if ((threadIdx.x & 31) == 0 && sum) atomicAdd(&st->v[idx], static_cast<unsigned long long>(sum));
 }
 
-// Path of global step index i: guide by the step index's high bits, then a
-// short forward scan of cum_steps.
-__device__ __forceinline__ uint32_t path_of_step(const DevGraph& g, uint64_t i) {
+// Path of global step index i with its base (cum_steps[p]) and length:
+// guide by the step index's high bits, then the guided path's constants in
+// one 64-byte line (PathConst); a short forward scan only when the guide's
+// bucket straddles a path end. Two dependent loads, not guide -> cum -> pc.
+// With want_z (a cooling unit) the path's Zipf support and alias-table
+// offset come from the same line in the same round trip.
+template <typename UX>
+__device__ __forceinline__ uint32_t path_of_step(const DevGraph& g, UX i, bool want_z, UX& base, UX& n,
+                                                 uint32_t& zn, uint64_t& zt) {
     uint32_t p = __ldg(g.sguide + (i >> g.sguide_shift));
-    while (__ldg(g.cum + p + 1) <= i) ++p;
+    const PathConst* c = g.pc + p;
+    base = static_cast<UX>(__ldg(&c->base));
+    n = static_cast<UX>(__ldg(&c->n));
+    if (want_z) {
+        zn = static_cast<uint32_t>(__ldg(&c->zn));
+        zt = __ldg(&c->ztab);
+    }
+    while (i - base >= n) {  // i >= base always: the guide never overshoots
+        c = g.pc + ++p;
+        base = static_cast<UX>(__ldg(&c->base));
+        n = static_cast<UX>(__ldg(&c->n));
+        if (want_z) {
+            zn = static_cast<uint32_t>(__ldg(&c->zn));
+            zt = __ldg(&c->ztab);
+        }
+    }
     return p;
 }
 
@@ -181,10 +202,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         uint32_t p = 0;
         UX pbase = 0;
         SX n = 0;
+        uint32_t zn = 0;
+        uint64_t zt = 0;
         if (active) {
-            p = path_of_step(g, gi);
-            pbase = static_cast<UX>(__ldg(g.cum + p));
-            n = static_cast<SX>(static_cast<UX>(__ldg(g.cum + p + 1)) - pbase);
+            UX len;
+            p = path_of_step<UX>(g, gi, cooling, pbase, len, zn, zt);
+            n = static_cast<SX>(len);
         }
         // Shared partner draws. Uniform batches (pair_window >= 1): lane 0
         // draws one position w0 on its path; every uniform lane on that path
@@ -222,8 +245,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const SX i = static_cast<SX>(gi - pbase);
         SX j;
         if (cooling) {
-            const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
-            const uint64_t zt = __ldg(&g.pc[p].ztab);
             const SX k = static_cast<SX>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
             const SX sign = (shared ? (tag >> 31) : ((coins >> 1) & 1u)) ? 1 : -1;
             j = i + sign * k;
