@@ -40,6 +40,34 @@ struct Xo {
     __device__ __forceinline__ uint64_t below(uint64_t n) { return __umul64hi(next(), n); }
 };
 
+// The same generator with its state in shared memory (four 32-lane
+// columns per warp, one u64 per lane each: conflict-free 8-byte accesses),
+// for kernels whose register budget is the binding limit: the state costs
+// one 32-bit address instead of eight registers held across the loop.
+struct XoSmem {
+    uint64_t* s;  // lane's word of column 0; column w at s + 32 * w
+
+    __device__ __forceinline__ uint64_t next() {
+        uint64_t a = s[0], b = s[32], c = s[64], d = s[96];
+        const uint64_t out = a + d;
+        const uint64_t t = b << 17;
+        c ^= a;
+        d ^= b;
+        b ^= c;
+        a ^= d;
+        c ^= t;
+        d = (d << 45) | (d >> 19);
+        s[0] = a;
+        s[32] = b;
+        s[64] = c;
+        s[96] = d;
+        return out;
+    }
+    __device__ __forceinline__ double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    __device__ __forceinline__ bool coin() { return (next() >> 63) != 0; }
+    __device__ __forceinline__ uint64_t below(uint64_t n) { return __umul64hi(next(), n); }
+};
+
 __host__ __device__ __forceinline__ uint64_t splitmix_next(uint64_t& st) {
     uint64_t z = (st += kPhi);
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -388,14 +416,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // apply_endpoint_update (engine.cpp:276-306) on the Hogwild store, without
 // calls into IEEE slow paths. Returns 1 if applied.
-template <typename T>
+template <typename T, typename R>
 __device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                              double d_ref, double eta, Xo& r, uint64_t pol, double vix,
+                                              double d_ref, double eta, R& r, uint64_t pol, double vix,
                                               double viy, double vjx, double vjy);
 
-template <typename T>
+template <typename T, typename R>
 __device__ __forceinline__ uint32_t hog_update_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                               double d_ref, double eta, Xo& r, uint64_t pol) {
+                                               double d_ref, double eta, R& r, uint64_t pol) {
     if (!(d_ref > 0.0)) return 0;
     double vix, viy, vjx, vjy;
     CoordHint<T>::get(coords, ni, ei, pol, vix, viy);
@@ -405,26 +433,26 @@ __device__ __forceinline__ uint32_t hog_update_t(void* coords, uint32_t ni, int 
 
 // hog_apply_t that also returns the new v_i (warp-shuffle reuse keeps
 // updating the same i endpoint).
-template <typename T, bool kGivenAnchors = false>
+template <typename T, bool kGivenAnchors = false, typename R>
 __device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                                 double d_ref, double eta, Xo& r, uint64_t pol, double& vix,
+                                                 double d_ref, double eta, R& r, uint64_t pol, double& vix,
                                                  double& viy, double vjx, double vjy, double anc_i = 0.0,
                                                  double anc_j = 0.0);
 
 // The arithmetic and write-back half of hog_update_t, on endpoint values the
 // caller loaded (d_ref > 0).
-template <typename T>
+template <typename T, typename R>
 __device__ __forceinline__ uint32_t hog_apply_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                              double d_ref, double eta, Xo& r, uint64_t pol, double vix,
+                                              double d_ref, double eta, R& r, uint64_t pol, double vix,
                                               double viy, double vjx, double vjy) {
     return hog_apply_io_t<T>(coords, ni, ei, nj, ej, d_ref, eta, r, pol, vix, viy, vjx, vjy);
 }
 
 // kGivenAnchors (anchored store only): the caller holds both nodes' block
 // anchors, so the write-back does not re-read them.
-template <typename T, bool kGivenAnchors>
+template <typename T, bool kGivenAnchors, typename R>
 __device__ __forceinline__ uint32_t hog_apply_io_t(void* coords, uint32_t ni, int ei, uint32_t nj, int ej,
-                                                 double d_ref, double eta, Xo& r, uint64_t pol, double& vix,
+                                                 double d_ref, double eta, R& r, uint64_t pol, double& vix,
                                                  double& viy, double vjx, double vjy, double anc_i,
                                                  double anc_j) {
     double mu = eta * rcp_nr(d_ref * d_ref);

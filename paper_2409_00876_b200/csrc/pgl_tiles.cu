@@ -81,7 +81,7 @@ struct AsyncRes {  // async pipeline: a resolved update, waiting for its endpoin
 
 // shared memory of the async pipeline with lookahead L, 256-thread blocks;
 // the anchored store adds the two endpoints' block anchors per update
-constexpr size_t async_smem_bytes(int L, bool anchored) {
+__host__ __device__ constexpr size_t async_smem_bytes(int L, bool anchored) {
     return L == 0 ? 0
                   : static_cast<size_t>(8 * 32) *
                         ((2 * L + 1) * (2 * sizeof(StepRec) + sizeof(uint32_t)) +
@@ -114,7 +114,26 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     const uint32_t lane = threadIdx.x & 31;
     if (warp >= a.n_warps) return;
 
-    Xo r{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
+    // async pipeline on the anchored store: the generator state lives in
+    // shared memory after the pipeline's slots -- the register budget binds
+    // that kernel (config 3: +1.3%; the FP64 store measured 3% slower)
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    constexpr bool kAnch = std::is_same_v<T, AnchF32>;
+    constexpr bool kSmemRng = kAsync != 0 && kAnch;
+    using Rng = std::conditional_t<kSmemRng, XoSmem, Xo>;
+    Rng r;
+    if constexpr (kSmemRng) {
+        constexpr size_t kRngOff = async_smem_bytes(kAsync, kAnch);
+        uint64_t* col = reinterpret_cast<uint64_t*>(dyn_smem + kRngOff) +
+                        (threadIdx.x >> 5) * 128 + lane;
+        col[0] = rng.s0[tid];
+        col[32] = rng.s1[tid];
+        col[64] = rng.s2[tid];
+        col[96] = rng.s3[tid];
+        r.s = col;
+    } else {
+        r = Xo{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
+    }
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = a.record_hint ? policy_evict_normal() : policy_evict_first();
     const UX S = static_cast<UX>(g.total_steps);
@@ -408,7 +427,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         constexpr int kWarps = 8;  // 256-thread blocks
         // dynamic shared memory (async_smem_bytes): [kRS] record pairs and
         // selection flags, [kCS] endpoint pairs and resolved updates
-        extern __shared__ __align__(16) unsigned char dyn_smem[];
         auto* s_ri = reinterpret_cast<StepRec(*)[kWarps][32]>(dyn_smem);
         auto* s_rj = s_ri + kRS;
         auto* s_vi = reinterpret_cast<uint4(*)[kWarps][32]>(s_rj + kRS);  // raw 16-byte copies (Coord<T>::decode)
@@ -416,7 +434,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         auto* s_res = reinterpret_cast<AsyncRes(*)[kWarps][32]>(s_vj + kCS);
         auto* s_fl = reinterpret_cast<uint32_t(*)[kWarps][32]>(s_res + kCS);
         // anchored store: block anchors of i and j, copied beside the records
-        constexpr bool kAnch = std::is_same_v<T, AnchF32>;
         auto* s_ai = reinterpret_cast<double(*)[kWarps][32]>(s_fl + kRS);
         auto* s_aj = s_ai + kCS;
         const int wib = static_cast<int>(threadIdx.x >> 5);
@@ -515,10 +532,17 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
     }
 
-    rng.s0[tid] = r.a;
-    rng.s1[tid] = r.b;
-    rng.s2[tid] = r.c;
-    rng.s3[tid] = r.d;
+    if constexpr (kSmemRng) {
+        rng.s0[tid] = r.s[0];
+        rng.s1[tid] = r.s[32];
+        rng.s2[tid] = r.s[64];
+        rng.s3[tid] = r.s[96];
+    } else {
+        rng.s0[tid] = r.a;
+        rng.s1[tid] = r.b;
+        rng.s2[tid] = r.c;
+        rng.s3[tid] = r.d;
+    }
     flush_stat(stats, 2, applied);
     flush_stat(stats, 4, b_first);
     flush_stat(stats, 5, b_first_cool);
@@ -553,7 +577,9 @@ const void* tiles_fn(int variant, bool k32) {
 }
 
 size_t tiles_smem(int variant, int coord_kind) {
-    return async_smem_bytes(variant == 5 || variant == 6 ? 1 : 0, coord_kind == PGL_COORD_F32_ANCHORED);
+    const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
+    // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
+    return async ? async_smem_bytes(1, anch) + (anch ? 256 * 4 * sizeof(uint64_t) : 0) : 0;
 }
 
 const void* tiles_fn_kind(int coord_kind, int variant, bool k32) {
