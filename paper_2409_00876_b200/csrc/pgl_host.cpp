@@ -736,6 +736,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     // plus one alias table per distinct Zipf support for the Hogwild kernel.
     std::vector<PathConst> pcs(G->n_paths);
     std::vector<ZipfAlias> tables;
+    uint32_t zdef_n = 1;
+    uint64_t zdef_tab = 0;
     {
         uint64_t base = 0;
         struct Memo {
@@ -758,6 +760,18 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             }
             pcs[p] = PathConst{base, n, zn, it->k[0], it->k[1], it->k[2], it->off};
             base += n;
+        }
+        // the support (and alias table) carrying the most steps
+        uint64_t best = 0;
+        for (const Memo& m : memo) {
+            uint64_t steps = 0;
+            for (uint32_t p = 0; p < G->n_paths; ++p)
+                if (pcs[p].zn == m.zn) steps += pcs[p].n;
+            if (steps > best) {
+                best = steps;
+                zdef_n = static_cast<uint32_t>(m.zn);
+                zdef_tab = m.off;
+            }
         }
     }
     G->pc.alloc(pcs.size());
@@ -858,6 +872,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.record_hint = ext.record_hint;
             a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : kHopLanes;
             a.reuse_shuffle = ext.reuse_shuffle ? 1 : 0;
+            a.zdef_n = zdef_n;
+            a.zdef_tab = zdef_tab;
         }
         if (kind == PGL_COORD_F32_ANCHORED && it > 0) launch_reanchor(coords, V, G->stream);
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));

@@ -97,6 +97,8 @@ struct IterArgs {
     uint32_t record_hint; // 0 = records evict_first in L2, 1 = evict_normal
     uint32_t hop_lanes;   // lanes sharing one Zipf hop (pair_window 3): 1..32, power of two
     uint32_t reuse_shuffle;  // drf > 1 extras by warp-shuffle reuse (paper §7.4) instead of endpoint combos
+    uint32_t zdef_n;      // the Zipf support covering the most steps, and its alias-table
+    uint64_t zdef_tab;    //   offset: read speculatively by k_sgd_tiles' cooling units
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].

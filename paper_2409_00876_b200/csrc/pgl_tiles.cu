@@ -218,6 +218,18 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const UX i0 = unit_i0;                 // first step of the unit, q0 mod S (warp-uniform)
         UX gi = i0 + lane;
         while (gi >= S) gi -= S;               // the unit wraps at the end of a pass (S < 32: repeatedly)
+        // The group leaders draw before the path lookup (a draw that turns
+        // out unused is simply discarded), so that in a cooling unit every
+        // lane can start the alias-table read for the most common Zipf
+        // support (IterArgs::zdef_*) while its path constants are in flight;
+        // the path's own support replaces it when they differ.
+        const bool win_lead = lane == 0 && !cooling && a.pair_window != 0;
+        const bool hop_lead = (lane & (a.hop_lanes - 1)) == 0 && cooling && a.pair_window == 3;
+        const int lead = cooling ? static_cast<int>(lane & ~(a.hop_lanes - 1)) : 0;
+        uint64_t draw = (win_lead || hop_lead) ? r.next() : 0;
+        draw = __shfl_sync(kFull, draw, lead);
+        uint32_t kspec = 0;
+        if (cooling && a.pair_window == 3) kspec = static_cast<uint32_t>(zipf_alias(g.zalias + a.zdef_tab, a.zdef_n, draw));
         uint32_t p = 0;
         UX pbase = 0;
         SX n = 0;
@@ -239,19 +251,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         // consecutive steps: coalesced record loads and neighbouring
         // coordinates instead of one random line per lane.
         // tag: bits 0-28 path, 29 leader was cooling, 30 draw valid, 31 sign
-        uint64_t draw = 0;
         uint32_t tag = p;
-        {
-            const bool win_lead = lane == 0 && !cooling && a.pair_window != 0;
-            const bool hop_lead = (lane & (a.hop_lanes - 1)) == 0 && cooling && a.pair_window == 3;
-            if (active && n >= 2 && (win_lead || hop_lead)) {
-                draw = r.next();
-                tag |= (1u << 30) | (cooling ? (1u << 29) : 0u);
-                if (cooling) tag |= ((coins >> 1) & 1u) << 31;
-            }
+        if (active && n >= 2 && (win_lead || hop_lead)) {
+            tag |= (1u << 30) | (cooling ? (1u << 29) : 0u);
+            if (cooling) tag |= ((coins >> 1) & 1u) << 31;
         }
-        const int lead = cooling ? static_cast<int>(lane & ~(a.hop_lanes - 1)) : 0;
-        draw = __shfl_sync(kFull, draw, lead);
         tag = __shfl_sync(kFull, tag, lead);
         const bool shared = ((tag >> 30) & 1) && ((tag >> 29) & 1) == (cooling ? 1u : 0u) && (tag & 0x1FFFFFFFu) == p;
         // the unit's records (one coalesced 512-byte load), issued after the
@@ -264,7 +268,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const SX i = static_cast<SX>(gi - pbase);
         SX j;
         if (cooling) {
-            const SX k = static_cast<SX>(zipf_alias(g.zalias + zt, zn, shared ? draw : r.next()));
+            const SX k = static_cast<SX>(
+                shared ? (zn == a.zdef_n && zt == a.zdef_tab ? kspec : zipf_alias(g.zalias + zt, zn, draw))
+                       : zipf_alias(g.zalias + zt, zn, r.next()));
             const SX sign = (shared ? (tag >> 31) : ((coins >> 1) & 1u)) ? 1 : -1;
             j = i + sign * k;
             if (j < 0 || j >= n) {
