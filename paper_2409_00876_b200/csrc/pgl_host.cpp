@@ -389,6 +389,8 @@ struct pgl_graph {
     DevBuf<uint32_t> sguide;
     uint32_t sguide_bits = 0, sguide_shift = 0;
     DevBuf<PathConst> pc;
+    DevBuf<uint4> fguide;                // per-layout path guide with inline constants (k_sgd_tiles)
+    uint32_t fguide_shift = 0;
     DevBuf<ZipfAlias> zalias;
     uint32_t guide_bits = 8;
     DevBuf<double> coords64;             // [4V] FP64 layout / staging
@@ -404,7 +406,7 @@ struct pgl_graph {
         stream = st;
         step.s = cum.s = stream;
         guide.s = sguide.s = stream;
-        pc.s = stream;
+        pc.s = fguide.s = stream;
         zalias.s = stream;
         coords64.s = stream;
         coords32.s = stream;
@@ -420,6 +422,7 @@ struct pgl_graph {
         guide.release();
         sguide.release();
         pc.release();
+        fguide.release();
         zalias.release();
         coords64.release();
         coords32.release();
@@ -777,6 +780,39 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     G->pc.alloc(pcs.size());
     PGL_CUDA(cudaMemcpyAsync(G->pc.p, pcs.data(), pcs.size() * sizeof(PathConst), cudaMemcpyHostToDevice,
                              G->stream));
+    // Path guide with the constants inline, for k_sgd_tiles on graphs with
+    // S < 2^30: bucket b of the step index's top bits -> {base, |p|, p | flags}
+    // where flag 31 = the bucket straddles a path end (scan PathConst as
+    // usual) and flag 30 = the path's Zipf support is zdef: one load resolves
+    // the path, its base and length, and whether the speculative alias read
+    // applies. ~8 buckets per path, 2^10-2^13 entries of 16 bytes.
+    std::vector<uint4> fg;
+    {
+        const uint64_t S = G->sum.total_steps;
+        uint32_t L = 1;
+        while ((1ULL << L) < std::max<uint64_t>(S, 2)) ++L;
+        uint32_t fb = 10;
+        while ((1u << fb) < 8u * std::max<uint32_t>(G->n_paths, 1) && fb < 13) ++fb;
+        fb = std::min(fb, L);
+        G->fguide_shift = L - fb;
+        fg.assign(1u << fb, uint4{0, 0, 1u << 31, 0});
+        if (S < (1ULL << 30) && G->n_paths) {
+            uint32_t p = 0;
+            for (uint64_t b = 0; b < fg.size(); ++b) {
+                const uint64_t first = b << G->fguide_shift;
+                if (first >= S) break;
+                const uint64_t last = std::min<uint64_t>(((b + 1) << G->fguide_shift) - 1, S - 1);
+                while (pcs[p].base + pcs[p].n <= first) ++p;
+                const bool straddle = pcs[p].base + pcs[p].n <= last;
+                const bool zd = pcs[p].zn == zdef_n && pcs[p].ztab == zdef_tab;
+                fg[b] = uint4{static_cast<uint32_t>(pcs[p].base), static_cast<uint32_t>(pcs[p].n),
+                              p | (straddle ? 1u << 31 : 0u) | (zd ? 1u << 30 : 0u), 0};
+            }
+        }
+        G->fguide.alloc(fg.size());
+        PGL_CUDA(cudaMemcpyAsync(G->fguide.p, fg.data(), fg.size() * sizeof(uint4), cudaMemcpyHostToDevice,
+                                 G->stream));
+    }
     G->zalias.alloc(std::max<size_t>(tables.size(), 1));
     if (!tables.empty())
         PGL_CUDA(cudaMemcpyAsync(G->zalias.p, tables.data(), tables.size() * sizeof(ZipfAlias),
@@ -874,6 +910,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.reuse_shuffle = ext.reuse_shuffle ? 1 : 0;
             a.zdef_n = zdef_n;
             a.zdef_tab = zdef_tab;
+            a.fguide = G->fguide.p;
+            a.fguide_shift = G->fguide_shift;
         }
         if (kind == PGL_COORD_F32_ANCHORED && it > 0) launch_reanchor(coords, V, G->stream);
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));

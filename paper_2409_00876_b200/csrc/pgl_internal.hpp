@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector_types.h>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -99,6 +100,8 @@ struct IterArgs {
     uint32_t reuse_shuffle;  // drf > 1 extras by warp-shuffle reuse (paper §7.4) instead of endpoint combos
     uint32_t zdef_n;      // the Zipf support covering the most steps, and its alias-table
     uint64_t zdef_tab;    //   offset: read speculatively by k_sgd_tiles' cooling units
+    const uint4* fguide;  // path guide with inline constants (S < 2^30), see graph_layout
+    uint32_t fguide_shift;
 };
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].

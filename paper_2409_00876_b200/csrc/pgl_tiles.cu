@@ -72,6 +72,40 @@ __device__ __forceinline__ uint32_t path_of_step(const DevGraph& g, UX i, bool w
     return p;
 }
 
+// k32 graphs: one 16-byte guide entry gives the path, its base and length
+// and whether its Zipf support is the speculated one (zdef); only a bucket
+// that straddles a path end falls back to the PathConst scan.
+template <typename UX>
+__device__ __forceinline__ uint32_t path_of_step_fat(const DevGraph& g, const IterArgs& a, UX i, bool want_z,
+                                                     UX& base, UX& n, uint32_t& zn, uint64_t& zt, bool& zdef) {
+    const uint4 e = __ldg(a.fguide + (i >> a.fguide_shift));
+    uint32_t p = e.z & 0x3FFFFFFFu;
+    if (!(e.z >> 31)) {
+        base = static_cast<UX>(e.x);
+        n = static_cast<UX>(e.y);
+        zdef = (e.z >> 30) & 1u;
+        if (want_z && !zdef) {
+            zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
+            zt = __ldg(&g.pc[p].ztab);
+        }
+        return p;
+    }
+    const PathConst* c = g.pc + p;
+    base = static_cast<UX>(__ldg(&c->base));
+    n = static_cast<UX>(__ldg(&c->n));
+    while (i - base >= n) {
+        c = g.pc + ++p;
+        base = static_cast<UX>(__ldg(&c->base));
+        n = static_cast<UX>(__ldg(&c->n));
+    }
+    if (want_z) {
+        zn = static_cast<uint32_t>(__ldg(&c->zn));
+        zt = __ldg(&c->ztab);
+    }
+    zdef = zn == a.zdef_n && zt == a.zdef_tab;
+    return p;
+}
+
 // Stage A product for one lane: its step i (record in flight), its partner j
 // (record in flight when outside the unit) and the coins.
 struct AsyncRes {  // async pipeline: a resolved update, waiting for its endpoints
@@ -235,9 +269,15 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         SX n = 0;
         uint32_t zn = 0;
         uint64_t zt = 0;
+        bool zdef = false;
         if (active) {
             UX len;
-            p = path_of_step<UX>(g, gi, cooling, pbase, len, zn, zt);
+            if constexpr (k32) {
+                p = path_of_step_fat<UX>(g, a, gi, cooling, pbase, len, zn, zt, zdef);
+            } else {
+                p = path_of_step<UX>(g, gi, cooling, pbase, len, zn, zt);
+                zdef = zn == a.zdef_n && zt == a.zdef_tab;
+            }
             n = static_cast<SX>(len);
         }
         // Shared partner draws. Uniform batches (pair_window >= 1): lane 0
@@ -269,7 +309,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         SX j;
         if (cooling) {
             const SX k = static_cast<SX>(
-                shared ? (zn == a.zdef_n && zt == a.zdef_tab ? kspec : zipf_alias(g.zalias + zt, zn, draw))
+                shared ? (zdef ? kspec : zipf_alias(g.zalias + zt, zn, draw))
                        : zipf_alias(g.zalias + zt, zn, r.next()));
             const SX sign = (shared ? (tag >> 31) : ((coins >> 1) & 1u)) ? 1 : -1;
             j = i + sign * k;
