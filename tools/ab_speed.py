@@ -1,6 +1,6 @@
 """A/B throughput probe: layout kernel time and SPS for one config with the
 library named by PGL_B200_LIB (or the in-tree one).
-usage: python tools/ab_speed.py CONFIG [REPS] [PREC]"""
+usage: python tools/ab_speed.py CONFIG [REPS] [PREC] [VARIANT]   (CONFIG c1 c2 c3 c5)"""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -10,15 +10,18 @@ GEN = {"c1": (1, 9680, 8, 0.05), "c2": (1, 968000, 90, 0.05), "c3": (1, 9680000,
 name = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else P.COORD_AUTO
-g = P.generate_synthetic_pangenome(*GEN[name])
+variant = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+g = (P.generate_nested_pangenome(5, 200000, 500, 3, 0.05) if name == "c5"
+     else P.generate_synthetic_pangenome(*GEN[name]))
 dg = P.DeviceGraph(g)
 upd = 30 * 10 * g.total_steps()
-ext = P.LayoutExt(coord_precision=prec)
-dg.layout(P.LayoutConfig(n_iters=3), ext=ext, copy_out=False)
+ext = P.LayoutExt(coord_precision=prec, kernel_variant=variant)
+kw = {"zipf_space_max": 100000} if name == "c5" else {}
+dg.layout(P.LayoutConfig(n_iters=3, **kw), ext=ext, copy_out=False)
 out = []
 for k in range(reps):
-    dg.layout(P.LayoutConfig(global_seed=101 + k), ext=ext, copy_out=False)
+    dg.layout(P.LayoutConfig(global_seed=101 + k, **kw), ext=ext, copy_out=False)
     out.append(dg.timing().kernel_ms)
 r = dg.stress(7, 20)
-print(json.dumps({"lib": os.environ.get("PGL_B200_LIB", "tree"), "config": name, "kernel_ms": out,
+print(json.dumps({"lib": os.environ.get("PGL_B200_LIB", "tree"), "config": name, "variant": variant, "kernel_ms": out,
                   "gupd_best": upd / min(out) / 1e6, "sps20": r.mean}), flush=True)
