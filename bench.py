@@ -336,7 +336,10 @@ def run_ours(args, dist: Dist):
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     dist.barrier()
     e2e_val, _ = aggregate(dist, updates * e2e_steps, e2e_s * e2e_steps)
-    h2d = 16 * S + 8 * (g.n_paths + 1) + 48 * g.n_paths + 32 * g.n_nodes + 4 * (1 << 16)
+    # what pgl_layout_run uploads for a build_graph-made view: one u32 step
+    # word per step + u32 node lengths (records are rebuilt on the device),
+    # cum_steps, per-path constants, the initial layout, guide/alias tables
+    h2d = 4 * S + 4 * g.n_nodes + 8 * (g.n_paths + 1) + 64 * g.n_paths + 32 * g.n_nodes + 4 * (1 << 16)
     d2h = 32 * g.n_nodes + 64
 
     cpu = None

@@ -505,6 +505,72 @@ void upload_tables(pgl_graph* G, const std::vector<uint64_t>& cum) {
     PGL_CUDA(cudaStreamSynchronize(G->stream));
 }
 
+// Compact upload: one u32 word per step (node | reverse << 31, 4 bytes
+// instead of a 16-byte record) plus u32 node lengths; the device rebuilds
+// the offsets and records exactly as for a GFA (build_records_device).
+// Valid when the view is what build_graph makes (graph.cpp:38-50): every
+// step's seq_len is its node's length and offsets are the running sums.
+// Checked step by step while packing; returns false (nothing built) when a
+// view is not of that form, and pack_graph then uploads full records.
+bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector<uint64_t>& cum) {
+    const uint64_t S = G->sum.total_steps, V = v->n_nodes;
+    if (V >= (1ULL << 31) || S == 0) return false;
+    std::vector<uint32_t> len32(V);
+    for (uint64_t n = 0; n < V; ++n) {
+        if (v->node_len[n] > 0xFFFFFFFFull) return false;
+        len32[n] = static_cast<uint32_t>(v->node_len[n]);
+    }
+    DevBuf<uint32_t> dlen, dsteps;
+    dlen.s = dsteps.s = G->stream;
+    dlen.alloc(std::max<uint64_t>(V, 1));
+    dsteps.alloc(S);
+    PGL_CUDA(cudaMemcpyAsync(dlen.p, len32.data(), V * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
+    const uint64_t kChunk = std::min<uint64_t>(1ULL << 23, S);  // <= 8 Mi steps = 32 MiB
+    G->pin.alloc(2 * kChunk * sizeof(uint32_t));
+    uint32_t* bufs[2] = {static_cast<uint32_t*>(G->pin.p), static_cast<uint32_t*>(G->pin.p) + kChunk};
+    cudaEvent_t done[2];
+    PGL_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    PGL_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    std::atomic<int> bad_node{0}, irregular{0};
+    const uint64_t n_chunks = (S + kChunk - 1) / kChunk;
+    for (uint64_t c = 0; c < n_chunks && !bad_node.load() && !irregular.load(); ++c) {
+        uint32_t* buf = bufs[c & 1];
+        if (c >= 2) PGL_CUDA(cudaEventSynchronize(done[c & 1]));
+        const uint64_t k0 = c * kChunk, k1 = std::min(S, k0 + kChunk);
+        parallel_for(k1 - k0, [&](uint64_t b, uint64_t e) {
+            uint64_t k = k0 + b;
+            uint32_t p = static_cast<uint32_t>(std::upper_bound(cum.begin(), cum.end(), k) - cum.begin() - 1);
+            bool odd = false, bad = false;
+            for (; k < k0 + e; ++k) {
+                while (k >= cum[p + 1]) ++p;
+                const pgl_path_step* ps = v->path_steps[p];
+                const uint64_t i = k - cum[p];
+                const pgl_path_step& st = ps[i];
+                if (st.node_id >= V) {
+                    bad = true;
+                    break;
+                }
+                const uint64_t want = i ? ps[i - 1].offset + ps[i - 1].seq_len : 0;
+                odd |= st.seq_len != len32[st.node_id] || st.offset != want || st.node_id >= (1u << 31);
+                buf[k - k0] = st.node_id | (st.orient ? 1u << 31 : 0u);
+            }
+            if (bad) bad_node.store(1, std::memory_order_relaxed);
+            if (odd) irregular.store(1, std::memory_order_relaxed);
+        });
+        PGL_CUDA(cudaMemcpyAsync(dsteps.p + k0, buf, (k1 - k0) * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                 G->stream));
+        PGL_CUDA(cudaEventRecord(done[c & 1], G->stream));
+    }
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+    if (bad_node.load()) raise(PGL_ERR_UNKNOWN_NODE, "path references a node outside the graph");
+    if (irregular.load()) return false;
+    build_records_device(dsteps.p, dlen.p, G->cum.p, G->n_paths, S, G->step.p, G->stream);
+    PGL_CUDA(cudaStreamSynchronize(G->stream));
+    return true;
+}
+
 void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
     const uint64_t S = G->sum.total_steps;
     const uint32_t P = v->n_paths;
@@ -514,6 +580,7 @@ void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
         if (v->path_total_len[p] >= (1ULL << 48))
             raise(PGL_ERR_INVALID_PARAMETER, "path longer than 2^48 nucleotides");
     upload_tables(G, cum);
+    if (pack_graph_compact(G, v, cum)) return;
 
     const uint64_t kChunk = std::min<uint64_t>(1ULL << 22, std::max<uint64_t>(S, 1));  // <= 4 Mi steps = 64 MiB
     G->pin.alloc(2 * kChunk * sizeof(StepRec));

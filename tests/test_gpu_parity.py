@@ -617,3 +617,25 @@ def test_long_nodes_hogwild_converges(pgl, oracle, gpu):
         out = pgl.run_layout(g, pgl.LayoutConfig(global_seed=3), ext=pgl.LayoutExt(kernel_variant=variant))
         assert np.isfinite(out).all()
         assert oracle.sps(go, out, 20).mean < init
+
+
+def test_index_from_view_offsets_when_not_prefix_sums(pgl, gpu):
+    """pgl_graph_create uploads one u32 word per step and rebuilds offsets on
+    the device when the view is what build_graph makes; a view whose offsets
+    are not the running sums (or whose seq_len differs from the node's) takes
+    the full-record path, so path_position still follows the view's own
+    PathStep.offset (graph.hpp:98-109)."""
+    g = pgl.build_graph([5, 3, 7, 2], [[(0, 0), (1, 1), (2, 0), (3, 1)], [(3, 0), (2, 1)]])
+    steps = [s.copy() for s in g.path_steps]
+    steps[0]["offset"] = [0, 9, 12, 30]          # gaps: not the running sums
+    odd = pgl.PangenomeGraph(g.node_len, steps)
+    for graph, arrs in ((g, g.path_steps), (odd, steps)):
+        want = []
+        for a in arrs:
+            for st in a:
+                near, far = int(st["offset"]), int(st["offset"]) + int(st["seq_len"])
+                want.append((far, near) if st["orient"] else (near, far))
+        with pgl.DeviceGraph(graph) as dg:
+            pos, nodes, _ = dg.export_index()
+        assert pos.tolist() == [list(w) for w in want]
+        assert nodes.tolist() == [int(st["node_id"]) for a in arrs for st in a]
