@@ -160,7 +160,8 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t kernel_variant;  /* tile kernel: 0 = auto; 1 = register pipeline, 2 CTAs/SM;
+    uint32_t kernel_variant;  /* tile kernel: 0 = auto (6 once the concurrency cap allows
+                                 8 warps per SM, else 1); 1 = register pipeline, 2 CTAs/SM;
                                  2 = register pipeline, 3 CTAs/SM; 5/6 = cp.async pipeline
                                  via shared memory, 4/3 CTAs/SM.
                                  i.i.d. kernel: 0 = 2 CTAs/SM, 1 = 3 CTAs/SM */

@@ -704,9 +704,9 @@ pgl_graph_view view_of(const pgl_graph* G) {
 constexpr uint32_t kHopLanes = 8;  // default lanes per shared Zipf hop
 
 // Tile-kernel variant (pgl_tiles.cu): auto = the asynchronous cp.async
-// pipeline at 3 CTAs/SM once the concurrency cap no longer binds (the graph
-// fills the GPU), else the register pipeline, whose shorter read-to-write
-// window keeps small graphs' layouts closest to the reference.
+// pipeline at 3 CTAs/SM once the concurrency cap allows 8 warps per SM,
+// else the register pipeline, whose shorter read-to-write window keeps
+// small graphs' layouts closest to the reference.
 int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
     int v = static_cast<int>(ext.kernel_variant & 15);
     const int force64 = static_cast<int>(ext.kernel_variant & 16);
