@@ -1,5 +1,5 @@
 """Short target for ncu: one layout of a config with few iterations.
-usage: python tools/prof_target.py CONFIG ITERS PREC [ORDER [FRONT_WARPS]]
+usage: python tools/prof_target.py CONFIG ITERS PREC [ORDER [FRONT_WARPS]]   (CONFIG c1 c2 c3 c5)
 ORDER: pgl_unit_order (0 auto = 1 spread)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -11,9 +11,11 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 order = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 fw = int(sys.argv[5]) if len(sys.argv) > 5 else 0
-g = P.generate_synthetic_pangenome(*cfgs[name])
+g = (P.generate_nested_pangenome(5, 200000, 500, 3, 0.05) if name == "c5"
+     else P.generate_synthetic_pangenome(*cfgs[name]))
+kw = {"zipf_space_max": 100000} if name == "c5" else {}
 dg = P.DeviceGraph(g)
-dg.layout(P.LayoutConfig(n_iters=iters), ext=P.LayoutExt(coord_precision=prec, unit_order=order, front_warps=fw),
-          copy_out=False)
+dg.layout(P.LayoutConfig(n_iters=iters, **kw),
+          ext=P.LayoutExt(coord_precision=prec, unit_order=order, front_warps=fw), copy_out=False)
 r = dg.stress(7, 10)
 print("done", dg.timing(), r.mean)
