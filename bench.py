@@ -1,32 +1,40 @@
 #!/usr/bin/env python
 """bench.py — PG-SGD layout throughput on B200 (BASELINE.json metric).
 
-Workload (N=1): config 2 of BASELINE.json, the synthetic 1M-node, 90-path
-graph generate_synthetic_pangenome(1, 968000, 90, 0.05) (1,000,240 nodes,
-87,114,705 path steps), LayoutConfig{} defaults (30 iterations, theta 0.99,
-Zipf window 1000, batch 32, drf = srf = 1). One bench step = one full
-run_layout of that graph: 30 x 10 x sum|p| = 2.61e10 attempted updates.
+Workload (N=1): config 3 of BASELINE.json, the north star's chr1-scale
+synthetic graph generate_synthetic_pangenome(1, 9680000, 90, 0.05)
+(10,002,606 nodes, 871,194,136 path steps), LayoutConfig{} defaults (30
+iterations, theta 0.99, Zipf window 1000, batch 32, drf = srf = 1). One bench
+step = one full run_layout of that graph: 30 x 10 x sum|p| = 2.61e11
+attempted updates. (--config c1|c2|c5 select the other single-GPU configs.)
 
   value  : updates/s with the packed graph resident in HBM; device time from
            CUDA events on the library's stream (init upload -> last SGD
            kernel), L2 flushed between steps.
   e2e    : updates/s through the C-ABI drop-in pgl_layout_run with HOST
            buffers: pack + H2D of the graph and initial layout, 30 kernels,
-           D2H of the coordinates, every step (host wall, synchronised).
-  roofline: k_sgd_tiles, algorithmic bytes per update = the payload one
-           update must move: two 16-byte step records (i, j) + two endpoint
-           reads + two endpoint write-backs (16 B each in f64, 8 B in f32)
-           = 96 B (f64) / 64 B (f32), x updates per launch / mean launch
-           time, against MEASURED_PEAKS.json hbm_gbs. (SURVEY.md §8d's 192 B
-           = six random 32-byte sectors priced the reference's i.i.d. access
-           pattern; the tile sampler's coalesced unit/window/hop loads move
-           less than that, so the payload is the honest denominator.)
+           D2H of the coordinates, every step (host wall, synchronised);
+           h2d/d2h bytes are the library's own copy counters
+           (pgl_transfer_bytes) around the timed calls.
+  roofline: k_sgd_tiles, bound "hbm": achieved = the DRAM bytes one launch
+           moves (dram__bytes_read.sum + dram__bytes_write.sum of the
+           committed ncu --set full capture of this kernel on this config,
+           profiles/ncu_traffic.json) / the live mean launch time, against
+           MEASURED_PEAKS.json hbm_gbs. The payload model (two 16-byte step
+           records + two endpoint reads + two write-backs = 96 B f64 / 64 B
+           f32 per update) is reported beside it as "payload"; SURVEY.md
+           §8d's 192 B = six random sectors prices the reference's i.i.d.
+           access pattern and does not apply to the tile sampler.
+  iid_sampler: one layout with the reference's i.i.d. selection
+           (SAMPLING_IID, k_sgd_hogwild) on the same graph, so the share of
+           the speed-up that comes from the tile sampler is explicit.
   cpu_baseline: the reference library itself (oracle/_ref, built from the
            reference sources), all host cores, on a bounded sample.
 
---gpus N (torchrun): every rank lays out its own copy of the graph (one
-chromosome per GPU, no collective: SURVEY.md §8e) -> weak scaling;
-value = all ranks' updates / max-over-ranks time.
+--gpus N (torchrun): every rank lays out its own chromosome-scale graph
+(config 3's shape, generator seed 1 + rank; one chromosome per GPU, no
+collective: SURVEY.md §8e) -> weak scaling; value = all ranks' updates /
+max-over-ranks time.
 --impl reference: times the reference CPU implementation (rank 0 only).
 """
 from __future__ import annotations
@@ -65,10 +73,14 @@ FALLBACK_HBM_GBS = 6650.0
 CONFIG_LAYOUT = {"c5": {"zipf_space_max": 100000}}  # LayoutConfig overrides per config
 
 
-def make_graph(P, config):
+def make_graph(P, config, rank=0):
+    """The config's graph; rank r > 0 of a multi-GPU run gets its own
+    chromosome of the same shape (generator seed + r)."""
+    args = CONFIGS[config]
+    args = (args[0] + rank,) + tuple(args[1:])
     if config == "c5":
-        return P.generate_nested_pangenome(*CONFIGS[config])
-    return P.generate_synthetic_pangenome(*CONFIGS[config])
+        return P.generate_nested_pangenome(*args)
+    return P.generate_synthetic_pangenome(*args)
 
 
 def parse():
@@ -77,7 +89,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--no-iid", action="store_true", help="skip the i.i.d.-sampler comparison layout")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--coord", choices=["auto", "f32", "f64", "anch"], default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,17 +212,19 @@ def hbm_peak():
 
 
 def ncu_traffic(config: str, coord: str):
-    """(dram bytes per SGD launch, cache/sector summary) from the committed
-    ncu --set full capture (profiles/ncu_traffic.json)."""
+    """(dram bytes per SGD launch, ncu ms of that launch, cache/sector
+    summary) from the committed ncu --set full capture
+    (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             e = json.load(f)[f"{config}_{coord}"]
     except (OSError, KeyError, ValueError):
-        return None, None
+        return None, None, None
     keys = ("l2_hit_pct", "l1_hit_pct", "ld_bytes_per_sector", "st_bytes_per_sector", "lsu_sectors_per_update",
-            "source")
-    return e.get("dram_bytes_per_launch"), {k: e[k] for k in keys if k in e}
+            "dram_bytes_per_update", "source")
+    return (e.get("dram_bytes_per_launch"), e.get("mixed_iteration", {}).get("ms"),
+            {k: e[k] for k in keys if k in e})
 
 
 # ---- CPU baseline: the reference itself --------------------------------------------
@@ -283,13 +298,15 @@ def run_ours(args, dist: Dist):
     torch.cuda.set_device(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
 
-    g = make_graph(P, args.config)
+    t_gen = time.perf_counter()
+    g = make_graph(P, args.config, dist.rank)
+    gen_s = time.perf_counter() - t_gen
     S = g.total_steps()
     cfg = P.LayoutConfig(global_seed=42 + dist.rank, **CONFIG_LAYOUT.get(args.config, {}))
     if args.coord == "auto":  # the library default: FP64 while it fits L2, anchored FP32 beyond
         args.coord = "f64" if 32 * g.n_nodes <= (64 << 20) else "anch"
-    ext = P.LayoutExt(coord_precision={"f64": P.COORD_F64, "f32": P.COORD_F32,
-                                       "anch": P.COORD_F32_ANCHORED}[args.coord])
+    coord_kind = {"f64": P.COORD_F64, "f32": P.COORD_F32, "anch": P.COORD_F32_ANCHORED}[args.coord]
+    ext = P.LayoutExt(coord_precision=coord_kind)
     updates = cfg.n_iters * (10 * S // cfg.srf) * cfg.drf
 
     dg = P.DeviceGraph(g, device=dev)
@@ -300,12 +317,13 @@ def run_ours(args, dist: Dist):
     clocks = Clocks(dev)
     clocks.start()
     dev_ms, kern_ms, launches = [], [], 0
+    st = P.RunStats()
     dist.barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
-        dg.layout(cfg, ext=ext, copy_out=False)
+        dg.layout(cfg, ext=ext, copy_out=False, stats=st)
         tm = dg.timing()
         dev_ms.append(tm.device_ms)
         kern_ms.append(tm.kernel_ms)
@@ -317,11 +335,28 @@ def run_ours(args, dist: Dist):
     step_s = sum(dev_ms) / 1e3 / args.steps
     value, t_max = aggregate(dist, updates * args.steps, step_s * args.steps)
     sgd_launch_ms = sum(kern_ms) / (args.steps * cfg.n_iters)
+    # the device's own counts for the last timed layout (DevStats)
+    stats = {"primary_steps": st.primary_steps, "updates_attempted": st.updates_attempted,
+             "updates_applied": st.updates_applied, "updates_skipped": st.updates_skipped,
+             "applied_fraction": st.updates_applied / max(st.updates_attempted, 1),
+             "device_counts_match": st.updates_attempted == updates
+             and st.updates_applied + st.updates_skipped == st.updates_attempted}
 
     # quality of the bench's own layout (device SPS kernel, spn 100, seed 7)
     sps, sps_ms = dg.stress(7, 100, return_ms=True)
     timing = dg.timing()
     info = dg.info()
+
+    # the reference's i.i.d. selection on the same graph (k_sgd_hogwild): the
+    # tile sampler's share of the speed-up
+    iid = None
+    if not args.no_iid:
+        dg.layout(cfg, ext=P.LayoutExt(coord_precision=coord_kind, sampling=P.SAMPLING_IID), copy_out=False)
+        ti = dg.timing()
+        iid_sps = dg.stress(7, 100)
+        iid = {"value": updates / (ti.device_ms / 1e3), "unit": UNIT, "layout_s": ti.device_ms / 1e3,
+               "launch_ms": ti.kernel_ms / cfg.n_iters, "kernel": "k_sgd_hogwild",
+               "sps_mean": iid_sps.mean, "sampling": "SAMPLING_IID (weighted_step_select i.i.d., graph.hpp:123-138)"}
     dg.close()
 
     # e2e through the C-ABI drop-in with host buffers
@@ -329,18 +364,18 @@ def run_ours(args, dist: Dist):
     P.run_layout(g, cfg, ext=ext, device=dev)  # warm
     dist.barrier()
     torch.cuda.synchronize()
+    h0, d0 = P.transfer_bytes()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         P.run_layout(g, cfg, ext=ext, device=dev)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
+    h1, d1 = P.transfer_bytes()
     dist.barrier()
     e2e_val, _ = aggregate(dist, updates * e2e_steps, e2e_s * e2e_steps)
-    # what pgl_layout_run uploads for a build_graph-made view: one u32 step
-    # word per step + u32 node lengths (records are rebuilt on the device),
-    # cum_steps, per-path constants, the initial layout, guide/alias tables
-    h2d = 4 * S + 4 * g.n_nodes + 8 * (g.n_paths + 1) + 64 * g.n_paths + 32 * g.n_nodes + 4 * (1 << 16)
-    d2h = 32 * g.n_nodes + 64
+    h2d, d2h = (h1 - h0) // e2e_steps, (d1 - d0) // e2e_steps  # counted by the library's copy wrappers
+    n_nodes, n_paths = g.n_nodes, g.n_paths
+    del g  # the CPU sample builds the reference's own copy of the graph
 
     cpu = None
     if dist.rank == 0 and not args.no_cpu_baseline and args.gpus == 1:
@@ -350,31 +385,41 @@ def run_ours(args, dist: Dist):
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
 
     peak, peak_src = hbm_peak()
-    bytes_per_launch = (10 * S // cfg.srf) * cfg.drf * BYTES_PER_UPDATE[args.coord]
-    achieved = bytes_per_launch / (sgd_launch_ms / 1e3) / 1e9
-    traffic, ncu_cache = ncu_traffic(args.config, args.coord)
+    payload = BYTES_PER_UPDATE[args.coord]
+    per_launch = (10 * S // cfg.srf) * cfg.drf
+    payload_gbs = per_launch * payload / (sgd_launch_ms / 1e3) / 1e9
+    traffic, ncu_ms, ncu_cache = ncu_traffic(args.config, args.coord)
+    if traffic:
+        achieved, model = traffic / (sgd_launch_ms / 1e3) / 1e9, "ncu-measured DRAM bytes per launch / live launch time"
+    else:
+        achieved, model = payload_gbs, "payload bytes (no ncu capture committed for this config)"
     if dist.rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD_NAME[args.config], "nodes": g.n_nodes, "paths": g.n_paths,
+            "config": {"workload": WORKLOAD_NAME[args.config], "nodes": n_nodes, "paths": n_paths,
                        "path_steps": S, "iters": cfg.n_iters, "updates_per_step": updates,
                        "coord_storage": args.coord, "parallelism": f"graph-per-GPU x{args.gpus} (no collective)",
                        "l2": "flushed between steps (256 MiB write); graph index 16 B/step > L2",
-                       "lanes": timing.device_threads, "grid": [timing.grid_blocks, timing.block_threads]},
+                       "lanes": timing.device_threads, "grid": [timing.grid_blocks, timing.block_threads],
+                       "generate_s": gen_s},
             "layout_wall_s": t_max / args.steps,
+            "run_stats": stats,
             "sps": {"mean": sps.mean, "ci": [sps.ci_low, sps.ci_high], "n": sps.n,
                     "method": "counter (GPU), seed 7, 100 samples/step", "kernel_ms": sps_ms},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "seconds_per_step": e2e_s, "api": "pgl_layout_run (C-ABI) from host PathStep arrays"},
+                    "seconds_per_step": e2e_s, "api": "pgl_layout_run (C-ABI) from host PathStep arrays",
+                    "bytes": "pgl_transfer_bytes deltas around the timed calls"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgd_tiles",
-                         "bytes_per_update": BYTES_PER_UPDATE[args.coord],
-                         "bytes_model": "payload: 2 step records + 2 endpoint reads + 2 endpoint writes",
-                         "launch_ms": sgd_launch_ms,
+                         "model": model, "launch_ms": sgd_launch_ms, "ncu_launch_ms": ncu_ms,
+                         "payload": {"bytes_per_update": payload, "achieved": payload_gbs,
+                                     "frac": payload_gbs / peak,
+                                     "model": "2 step records + 2 endpoint reads + 2 endpoint writes"},
                          "peak_source": peak_src, "ncu": ncu_cache},
+            "iid_sampler": iid,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clk,

@@ -83,6 +83,11 @@ int pgl_abi_version(void);
 /* Number of visible CUDA devices (0 when no GPU / no driver). Never fails. */
 int pgl_device_count(void);
 
+/* Bytes the library has copied host -> device and device -> host since it
+ * was loaded (every cudaMemcpy it issues, all devices): the e2e bench reads
+ * it around its timed calls. */
+int pgl_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+
 /* ---- configuration ------------------------------------------------------ */
 
 /* Field-for-field LayoutConfig (engine.hpp:13-23), same order and defaults.
@@ -179,7 +184,25 @@ typedef struct pgl_layout_ext {
                                  1 = warp-level data reuse (paper §7.4): extra updates pair
                                  this lane's i with another lane's partner, from registers */
     uint32_t _reserved[1];
+    struct pgl_layout_diag* diag; /* sampler diagnostics (Hogwild modes), NULL = off */
 } pgl_layout_ext;
+
+/* Sampler diagnostics, counted inside the Hogwild kernels while they run
+ * (they cost a few atomics per update, so measurements leave them off).
+ * Every member is optional. */
+typedef struct pgl_layout_diag {
+    uint32_t* primary_visits; /* host [total_steps]: how often each step was the primary step i,
+                                 summed over the run (the reference draws i i.i.d.,
+                                 graph.hpp:123-138; the tile sampler enumerates) */
+    uint64_t* zipf_draws;     /* host [zipf_draws_len]: histogram of the Zipf hops k drawn by
+                                 cooling selections (one count per draw, k >= len in the last
+                                 cell; ZipfSampler, rng.hpp:103-117) */
+    uint32_t zipf_draws_len;
+    uint32_t _pad;
+    uint64_t outcomes[4];     /* out: primary updates {uniform attempted, uniform applied,
+                                 cooling attempted, cooling applied} (the selection rules of
+                                 select_step_pair + apply_endpoint_update, test_engine.cpp:210-240) */
+} pgl_layout_diag;
 
 void pgl_layout_ext_default(pgl_layout_ext* ext);
 

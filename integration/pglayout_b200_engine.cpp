@@ -105,7 +105,19 @@ Layout run(const PangenomeGraph& g, const LayoutConfig& cfg, const IterationCall
     const pgl_layout_config c = to_c(cfg);
     pgl_layout_ext ext;
     pgl_layout_ext_default(&ext);
-    ext.mode = cfg.threads == 1 ? PGL_MODE_REPLAY : PGL_MODE_HOGWILD;
+    // threads = 1 is the reference's reproducible mode (engine.hpp:76-79). The
+    // bit-exact device replay of it runs one step at a time (~0.9 us/step), so
+    // it is used only while a run is small enough to finish in seconds
+    // (config 1, 2.3e7 updates: ~20 s; the reference's own suites, whose
+    // threads = 1 cases are all below this); larger threads = 1 runs go to the
+    // Hogwild kernels (not reproducible run to run, SPS-equivalent).
+    // PGLAYOUT_B200_MODE=replay forces replay at any size,
+    // PGLAYOUT_B200_REPLAY_MAX_UPDATES moves the threshold.
+    uint64_t replay_max = 32'000'000;
+    if (const char* m = std::getenv("PGLAYOUT_B200_REPLAY_MAX_UPDATES")) replay_max = std::strtoull(m, nullptr, 10);
+    const uint64_t updates = static_cast<uint64_t>(cfg.n_iters) * (total_update_steps(g) / std::max<uint32_t>(cfg.srf, 1)) *
+                             std::max<uint32_t>(cfg.drf, 1);
+    ext.mode = cfg.threads == 1 && updates <= replay_max ? PGL_MODE_REPLAY : PGL_MODE_HOGWILD;
     if (const char* m = std::getenv("PGLAYOUT_B200_MODE")) {
         if (!std::strcmp(m, "hogwild")) ext.mode = PGL_MODE_HOGWILD;
         if (!std::strcmp(m, "replay")) ext.mode = PGL_MODE_REPLAY;

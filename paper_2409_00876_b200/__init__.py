@@ -30,7 +30,7 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 __all__ = [
-    "LayoutConfig", "LayoutExt", "RunStats", "StressReport", "PangenomeGraph", "DeviceGraph",
+    "LayoutConfig", "LayoutExt", "LayoutDiag", "RunStats", "StressReport", "PangenomeGraph", "DeviceGraph",
     "Timing", "run_layout", "run_layout_reuse", "sampled_path_stress", "make_schedule",
     "init_layout", "build_graph", "generate_synthetic_pangenome", "layout_shards", "shard_plan",
     "device_count", "Error", "MODE_HOGWILD", "MODE_REPLAY", "COORD_F32", "COORD_F64",
@@ -73,7 +73,13 @@ class _Ext(C.Structure):
                 ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
                 ("sampling", C.c_uint32), ("unit_order", C.c_uint32), ("front_warps", C.c_uint32),
                 ("pair_window", C.c_uint32), ("record_hint", C.c_uint32), ("hop_lanes", C.c_uint32),
-                ("reuse_shuffle", C.c_uint32), ("_reserved", C.c_uint32 * 1)]
+                ("reuse_shuffle", C.c_uint32), ("_reserved", C.c_uint32 * 1),
+                ("diag", C.c_void_p)]
+
+
+class _Diag(C.Structure):
+    _fields_ = [("primary_visits", C.POINTER(C.c_uint32)), ("zipf_draws", C.POINTER(C.c_uint64)),
+                ("zipf_draws_len", C.c_uint32), ("_pad", C.c_uint32), ("outcomes", C.c_uint64 * 4)]
 
 
 class _PathStep(C.Structure):
@@ -123,12 +129,13 @@ EDGE_DTYPE = np.dtype({"names": ["from", "to", "from_end", "to_end"],
 
 _CB = C.CFUNCTYPE(C.c_int, C.c_uint32, _f64p, C.c_double, C.c_double, C.c_void_p)
 
-assert C.sizeof(_Cfg) == 56 and C.sizeof(_PathStep) == 24 and C.sizeof(_Ext) == 64
+assert C.sizeof(_Cfg) == 56 and C.sizeof(_PathStep) == 24 and C.sizeof(_Ext) == 72 and C.sizeof(_Diag) == 56
 
 _vp = C.c_void_p
 _sig = {
     "pgl_last_error": ([], C.c_char_p), "pgl_last_error_type": ([], C.c_int),
     "pgl_abi_version": ([], C.c_int), "pgl_device_count": ([], C.c_int),
+    "pgl_transfer_bytes": ([_u64p, _u64p], C.c_int),
     "pgl_layout_run": ([C.c_int, C.POINTER(_View), C.POINTER(_Cfg), C.POINTER(_Ext), C.c_int, _CB,
                         C.c_int, _vp, _f64p, C.POINTER(_Stats)], C.c_int),
     "pgl_graph_create": ([C.c_int, C.POINTER(_View), C.POINTER(_vp)], C.c_int),
@@ -266,6 +273,8 @@ class LayoutExt:
     record_hint: int = 0  # 0 evict_first, 1 evict_normal
     hop_lanes: int = 0  # lanes per shared Zipf hop (pair_window 3), 0 = auto
     reuse_shuffle: int = 0  # drf > 1 extras by warp-shuffle reuse (paper §7.4)
+    # sampler diagnostics (pgl_layout_diag), counted by the Hogwild kernels
+    diag: Optional["LayoutDiag"] = None
 
     def _c(self) -> _Ext:
         e = _Ext()
@@ -278,7 +287,35 @@ class LayoutExt:
         e.unit_order, e.front_warps = self.unit_order, self.front_warps
         e.pair_window, e.record_hint, e.hop_lanes = self.pair_window, self.record_hint, self.hop_lanes
         e.reuse_shuffle = self.reuse_shuffle
+        if self.diag is not None:
+            e.diag = C.addressof(self.diag._c())
         return e
+
+
+class LayoutDiag:
+    """Sampler diagnostics (pgl_layout_diag): per-step primary visit counts,
+    the histogram of Zipf hops drawn, and the primary updates' outcome counts
+    {uniform attempted, uniform applied, cooling attempted, cooling applied},
+    counted inside the Hogwild kernels. Pass as LayoutExt(diag=...); the
+    arrays are filled when the layout returns."""
+
+    def __init__(self, total_steps: int = 0, zipf_len: int = 0):
+        self.primary_visits = np.zeros(total_steps, np.uint32) if total_steps else None
+        self.zipf_draws = np.zeros(zipf_len, np.uint64) if zipf_len else None
+        self._s = _Diag()
+
+    def _c(self) -> "_Diag":
+        s = self._s
+        if self.primary_visits is not None:
+            s.primary_visits = self.primary_visits.ctypes.data_as(C.POINTER(C.c_uint32))
+        if self.zipf_draws is not None:
+            s.zipf_draws = self.zipf_draws.ctypes.data_as(C.POINTER(C.c_uint64))
+            s.zipf_draws_len = self.zipf_draws.size
+        return s
+
+    @property
+    def outcomes(self):
+        return [int(x) for x in self._s.outcomes]
 
 
 @dataclass
@@ -544,11 +581,18 @@ def _callback(on_iteration, n_nodes):
     return fn, 1
 
 
+def _check_diag(ext, total_steps):
+    d = ext.diag if ext is not None else None
+    if d is not None and d.primary_visits is not None and d.primary_visits.size != total_steps:
+        raise InvalidParameter("InvalidParameter: LayoutDiag.primary_visits needs total_steps entries")
+
+
 def _run(device, g, cfg, ext, reuse, on_iteration, stats, want_coords=True):
     cfg = cfg or LayoutConfig()
     out = np.zeros(4 * g.n_nodes)
     st = _Stats()
     cb, wants = _callback(on_iteration, g.n_nodes)
+    _check_diag(ext, g.total_steps())
     e = ext._c() if ext else None
     rc = _lib.pgl_layout_run(device, C.byref(g.view()), C.byref(cfg._c()),
                              C.byref(e) if e else None, int(reuse), cb, wants, None,
@@ -616,6 +660,13 @@ def device_count() -> int:
     return int(_lib.pgl_device_count())
 
 
+def transfer_bytes():
+    """(host->device, device->host) bytes the library has copied so far."""
+    h, d = C.c_uint64(0), C.c_uint64(0)
+    _check(_lib.pgl_transfer_bytes(C.byref(h), C.byref(d)))
+    return int(h.value), int(d.value)
+
+
 class DeviceGraph:
     """A graph packed and resident in HBM (pgl_graph_create): repeated layouts
     and stress evaluations without re-uploading the index."""
@@ -664,6 +715,8 @@ class DeviceGraph:
         out = np.zeros(4 * self.n_nodes) if copy_out else None
         st = _Stats()
         cb, wants = _callback(on_iteration, self.n_nodes)
+        if ext is not None and ext.diag is not None:
+            _check_diag(ext, self.info()["total_steps"])
         e = ext._c() if ext else None
         rc = _lib.pgl_graph_layout(self.h, C.byref(cfg._c()), C.byref(e) if e else None, int(reuse), cb,
                                    wants, None, out.ctypes.data_as(_f64p) if copy_out else None,
@@ -741,6 +794,8 @@ def layout_shards(graphs: Sequence[PangenomeGraph], cfgs: Sequence[LayoutConfig]
     secs = np.zeros(max(n, 1))
     assign = (C.c_int * max(n, 1))()
     st = (_Stats * max(n, 1))()
+    if ext is not None and ext.diag is not None:
+        raise InvalidParameter("InvalidParameter: LayoutDiag is per graph; not available for layout_shards")
     e = ext._c() if ext else None
     _check(_lib.pgl_layout_shards(len(devices), devs, n, views, cs, C.byref(e) if e else None,
                                   optr, st, secs.ctypes.data_as(_f64p), assign))

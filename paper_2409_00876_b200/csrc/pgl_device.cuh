@@ -14,6 +14,17 @@ namespace pgl {
 
 constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ULL;
 
+// diagnostics helpers (uniform branch on a kernel argument: free when off)
+__device__ __forceinline__ void diag_zipf(const IterArgs& a, uint64_t k) {
+    if (a.zhist != nullptr) atomicAdd(a.zhist + (k < a.zhist_len ? k : a.zhist_len - 1), 1ULL);
+}
+__device__ __forceinline__ void diag_outcome(const IterArgs& a, bool cooling, bool applied) {
+    if (a.outcomes != nullptr) {
+        atomicAdd(a.outcomes + (cooling ? 2 : 0), 1ULL);
+        if (applied) atomicAdd(a.outcomes + (cooling ? 3 : 1), 1ULL);
+    }
+}
+
 // ---- xoshiro256+ held in registers (rng.hpp:21-47) ------------------------
 
 struct Xo {

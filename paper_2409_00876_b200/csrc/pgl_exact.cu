@@ -213,7 +213,7 @@ void run_exact_stress(const DevGraph& g, const double* coords, pgl_stress_report
         if (n2 > static_cast<uint64_t>(kFoldBlock)) raise(PGL_ERR_INVALID_PARAMETER, "exact path stress: too many steps");
         k_exact_fold<<<1, kFoldBlock, 0, stream>>>(lvl2, n2, fin);
         PGL_CUDA(cudaGetLastError());
-        PGL_CUDA(cudaMemcpyAsync(&res[pass - 1], fin, sizeof(RowAcc), cudaMemcpyDeviceToHost, stream));
+        PGL_CUDA(copy_async(&res[pass - 1], fin, sizeof(RowAcc), cudaMemcpyDeviceToHost, stream));
         PGL_CUDA(cudaStreamSynchronize(stream));
         if (pass == 1) {
             const double sum = res[0].hi + res[0].lo;

@@ -464,7 +464,7 @@ void upload_tables(pgl_graph* G, const std::vector<uint64_t>& cum) {
     const uint32_t P = G->n_paths;
     G->step.alloc(S);
     G->cum.alloc(P + 1);
-    PGL_CUDA(cudaMemcpyAsync(G->cum.p, cum.data(), (P + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, G->stream));
+    PGL_CUDA(copy_async(G->cum.p, cum.data(), (P + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, G->stream));
 
     // guide table: bucket b of the top guide_bits of the selection draw
     // starts at pick floor(b * S / 2^bits); store the path containing it.
@@ -495,12 +495,12 @@ void upload_tables(pgl_graph* G, const std::vector<uint64_t>& cum) {
             sg[b] = static_cast<uint32_t>(std::min<uint64_t>(pth, P ? P - 1 : 0));
         }
         G->sguide.alloc(sg.size());
-        PGL_CUDA(cudaMemcpyAsync(G->sguide.p, sg.data(), sg.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+        PGL_CUDA(copy_async(G->sguide.p, sg.data(), sg.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                  G->stream));
         PGL_CUDA(cudaStreamSynchronize(G->stream));
     }
     G->guide.alloc(guide.size());
-    PGL_CUDA(cudaMemcpyAsync(G->guide.p, guide.data(), guide.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
+    PGL_CUDA(copy_async(G->guide.p, guide.data(), guide.size() * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              G->stream));
     PGL_CUDA(cudaStreamSynchronize(G->stream));
 }
@@ -524,7 +524,7 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
     dlen.s = dsteps.s = G->stream;
     dlen.alloc(std::max<uint64_t>(V, 1));
     dsteps.alloc(S);
-    PGL_CUDA(cudaMemcpyAsync(dlen.p, len32.data(), V * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
+    PGL_CUDA(copy_async(dlen.p, len32.data(), V * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
     const uint64_t kChunk = std::min<uint64_t>(1ULL << 23, S);  // <= 8 Mi steps = 32 MiB
     G->pin.alloc(2 * kChunk * sizeof(uint32_t));
     uint32_t* bufs[2] = {static_cast<uint32_t*>(G->pin.p), static_cast<uint32_t*>(G->pin.p) + kChunk};
@@ -557,7 +557,7 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
             if (bad) bad_node.store(1, std::memory_order_relaxed);
             if (odd) irregular.store(1, std::memory_order_relaxed);
         });
-        PGL_CUDA(cudaMemcpyAsync(dsteps.p + k0, buf, (k1 - k0) * sizeof(uint32_t), cudaMemcpyHostToDevice,
+        PGL_CUDA(copy_async(dsteps.p + k0, buf, (k1 - k0) * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                  G->stream));
         PGL_CUDA(cudaEventRecord(done[c & 1], G->stream));
     }
@@ -609,7 +609,7 @@ void pack_graph(pgl_graph* G, const pgl_graph_view* v) {
                                       static_cast<uint32_t>((ps >> 32) | ((pe >> 32) << 16))};
             }
         });
-        PGL_CUDA(cudaMemcpyAsync(G->step.p + k0, buf, (k1 - k0) * sizeof(StepRec), cudaMemcpyHostToDevice,
+        PGL_CUDA(copy_async(G->step.p + k0, buf, (k1 - k0) * sizeof(StepRec), cudaMemcpyHostToDevice,
                                  G->stream));
         PGL_CUDA(cudaEventRecord(done[c & 1], G->stream));
     }
@@ -684,8 +684,8 @@ pgl_graph* create_graph_gfa(int device, GfaGraph* gf) {
     dlen.s = dsteps.s = G->stream;
     dlen.alloc(std::max<uint64_t>(c.n_nodes, 1));
     dsteps.alloc(std::max<uint64_t>(sm.total_steps, 1));
-    PGL_CUDA(cudaMemcpyAsync(dlen.p, len32.data(), c.n_nodes * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
-    PGL_CUDA(cudaMemcpyAsync(dsteps.p, c.steps, sm.total_steps * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
+    PGL_CUDA(copy_async(dlen.p, len32.data(), c.n_nodes * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
+    PGL_CUDA(copy_async(dsteps.p, c.steps, sm.total_steps * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
     build_records_device(dsteps.p, dlen.p, G->cum.p, c.n_paths, sm.total_steps, G->step.p, G->stream);
     PGL_CUDA(cudaStreamSynchronize(G->stream));
     G->stats.alloc(8);
@@ -794,7 +794,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     PGL_CUDA(cudaEventCreate(&ev_begin));
     PGL_CUDA(cudaEventCreate(&ev_end));
     PGL_CUDA(cudaEventRecord(ev_begin, G->stream));
-    PGL_CUDA(cudaMemcpyAsync(G->coords64.p, hinit, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+    PGL_CUDA(copy_async(G->coords64.p, hinit, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
     void* coords = G->coords64.p;
     if (kind == PGL_COORD_F32) {
         G->coords32.alloc(4 * V);
@@ -849,7 +849,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         }
     }
     G->pc.alloc(pcs.size());
-    PGL_CUDA(cudaMemcpyAsync(G->pc.p, pcs.data(), pcs.size() * sizeof(PathConst), cudaMemcpyHostToDevice,
+    PGL_CUDA(copy_async(G->pc.p, pcs.data(), pcs.size() * sizeof(PathConst), cudaMemcpyHostToDevice,
                              G->stream));
     // Path guide with the constants inline, for k_sgd_tiles on graphs with
     // S < 2^30: bucket b of the step index's top bits -> {base, |p|, p | flags}
@@ -881,12 +881,12 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             }
         }
         G->fguide.alloc(fg.size());
-        PGL_CUDA(cudaMemcpyAsync(G->fguide.p, fg.data(), fg.size() * sizeof(uint4), cudaMemcpyHostToDevice,
+        PGL_CUDA(copy_async(G->fguide.p, fg.data(), fg.size() * sizeof(uint4), cudaMemcpyHostToDevice,
                                  G->stream));
     }
     G->zalias.alloc(std::max<size_t>(tables.size(), 1));
     if (!tables.empty())
-        PGL_CUDA(cudaMemcpyAsync(G->zalias.p, tables.data(), tables.size() * sizeof(ZipfAlias),
+        PGL_CUDA(copy_async(G->zalias.p, tables.data(), tables.size() * sizeof(ZipfAlias),
                                  cudaMemcpyHostToDevice, G->stream));
     PGL_CUDA(cudaMemsetAsync(G->stats.p, 0, 8 * sizeof(unsigned long long), G->stream));
 
@@ -940,6 +940,22 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (!replay) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, ext.l2_fetch_bytes ? ext.l2_fetch_bytes : 32);
     const uint64_t spi = 10 * G->sum.total_steps / cfg.srf;  // engine.cpp:197
     const DevGraph dg_ = G->dev();
+    // sampler diagnostics of the Hogwild kernels (pgl_layout_diag)
+    DevBuf<unsigned int> visits;
+    DevBuf<unsigned long long> zhist, outc;
+    visits.s = zhist.s = outc.s = G->stream;
+    if (ext.diag && !replay) {
+        if (ext.diag->primary_visits) {
+            visits.alloc(std::max<uint64_t>(G->sum.total_steps, 1));
+            PGL_CUDA(cudaMemsetAsync(visits.p, 0, G->sum.total_steps * sizeof(unsigned int), G->stream));
+        }
+        if (ext.diag->zipf_draws && ext.diag->zipf_draws_len) {
+            zhist.alloc(ext.diag->zipf_draws_len);
+            PGL_CUDA(cudaMemsetAsync(zhist.p, 0, ext.diag->zipf_draws_len * sizeof(unsigned long long), G->stream));
+        }
+        outc.alloc(4);
+        PGL_CUDA(cudaMemsetAsync(outc.p, 0, 4 * sizeof(unsigned long long), G->stream));
+    }
     DevStats* dstats = reinterpret_cast<DevStats*>(G->stats.p);
     std::vector<cudaEvent_t> ev(2 * cfg.n_iters);
     for (auto& e : ev) PGL_CUDA(cudaEventCreate(&e));
@@ -983,6 +999,13 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.zdef_tab = zdef_tab;
             a.fguide = G->fguide.p;
             a.fguide_shift = G->fguide_shift;
+            // rotate the enumeration's start every iteration: with srf not
+            // dividing 10, N mod S steps get one extra visit per pass
+            a.q_off = pr.below(std::max<uint64_t>(G->sum.total_steps, 1));
+            a.visits = visits.p;
+            a.zhist = zhist.p;
+            a.zhist_len = zhist.p ? ext.diag->zipf_draws_len : 0;
+            a.outcomes = outc.p;
         }
         if (kind == PGL_COORD_F32_ANCHORED && it > 0) launch_reanchor(coords, V, G->stream);
         PGL_CUDA(cudaEventRecord(ev[2 * it], G->stream));
@@ -998,7 +1021,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             if (cb_wants_coords) {
                 host_coords.resize(4 * V);
                 to_f64(G, kind);
-                PGL_CUDA(cudaMemcpyAsync(host_coords.data(), G->coords64.p, 4 * V * sizeof(double),
+                PGL_CUDA(copy_async(host_coords.data(), G->coords64.p, 4 * V * sizeof(double),
                                          cudaMemcpyDeviceToHost, G->stream));
                 cptr = host_coords.data();
             }
@@ -1029,22 +1052,36 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (aborted) raise(PGL_ERR_CALLBACK, "iteration callback requested abort");
 
     unsigned long long dst[8];
-    PGL_CUDA(cudaMemcpy(dst, G->stats.p, sizeof dst, cudaMemcpyDeviceToHost));
+    PGL_CUDA(copy_sync(dst, G->stats.p, sizeof dst, cudaMemcpyDeviceToHost));
     if (stats_out) {
+        // every field is a device count (DevStats); tests hold them to the
+        // reference's identities (test_engine.cpp:257-278)
         pgl_run_stats st{};
-        st.primary_steps = static_cast<uint64_t>(cfg.n_iters) * spi;
-        st.updates_attempted = st.primary_steps * cfg.drf;
+        st.primary_steps = dst[0];
+        st.updates_attempted = dst[1];
         st.updates_applied = dst[2];
-        st.updates_skipped = st.updates_attempted - dst[2];
+        st.updates_skipped = dst[3];
         st.batches_first_half = dst[4];
         st.batches_first_half_cooling = dst[5];
         st.batches_second_half = dst[6];
         st.batches_second_half_cooling = dst[7];
         *stats_out = st;
     }
+    if (ext.diag && !replay) {
+        if (visits.p)
+            PGL_CUDA(copy_async(ext.diag->primary_visits, visits.p, G->sum.total_steps * sizeof(unsigned int),
+                                     cudaMemcpyDeviceToHost, G->stream));
+        if (zhist.p)
+            PGL_CUDA(copy_async(ext.diag->zipf_draws, zhist.p,
+                                     ext.diag->zipf_draws_len * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                     G->stream));
+        PGL_CUDA(copy_async(ext.diag->outcomes, outc.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 G->stream));
+        PGL_CUDA(cudaStreamSynchronize(G->stream));
+    }
     if (out_coords) {
         to_f64(G, kind);
-        PGL_CUDA(cudaMemcpyAsync(out_coords, G->coords64.p, 4 * V * sizeof(double), cudaMemcpyDeviceToHost,
+        PGL_CUDA(copy_async(out_coords, G->coords64.p, 4 * V * sizeof(double), cudaMemcpyDeviceToHost,
                                  G->stream));
         PGL_CUDA(cudaStreamSynchronize(G->stream));
     }
@@ -1073,7 +1110,7 @@ void graph_stress(pgl_graph* G, const double* coords, uint64_t seed, uint32_t sp
     int f64;
     if (coords) {
         G->coords64.alloc(4 * V);
-        PGL_CUDA(cudaMemcpyAsync(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+        PGL_CUDA(copy_async(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
         dc = G->coords64.p;
         f64 = PGL_COORD_F64;
         G->layout_f64 = -1;  // the resident layout is overwritten
@@ -1097,7 +1134,7 @@ void graph_exact_stress(pgl_graph* G, const double* coords, pgl_stress_report* o
     const uint64_t V = G->n_nodes;
     if (coords) {
         G->coords64.alloc(4 * V);
-        PGL_CUDA(cudaMemcpyAsync(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+        PGL_CUDA(copy_async(G->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, G->stream));
         G->layout_f64 = -1;  // the resident layout is overwritten
     } else {
         if (G->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
@@ -1305,6 +1342,16 @@ Synthetic* generate_nested(uint64_t seed, uint64_t B, uint32_t n_paths, uint32_t
 
 struct pgl_synthetic : Synthetic {};
 
+namespace pgl {
+std::atomic<uint64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+void count_copy(cudaMemcpyKind kind, size_t bytes) {
+    if (kind == cudaMemcpyHostToDevice)
+        g_h2d_bytes.fetch_add(bytes, std::memory_order_relaxed);
+    else if (kind == cudaMemcpyDeviceToHost)
+        g_d2h_bytes.fetch_add(bytes, std::memory_order_relaxed);
+}
+}  // namespace pgl
+
 // ---- C ABI -----------------------------------------------------------------------
 
 extern "C" {
@@ -1312,6 +1359,12 @@ extern "C" {
 const char* pgl_last_error(void) { return t_err.c_str(); }
 int pgl_last_error_type(void) { return t_err_type; }
 int pgl_abi_version(void) { return PGL_ABI_VERSION; }
+
+int pgl_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = g_h2d_bytes.load(std::memory_order_relaxed);
+    if (d2h) *d2h = g_d2h_bytes.load(std::memory_order_relaxed);
+    return PGL_OK;
+}
 
 int pgl_device_count(void) {
     int n = 0;
@@ -1379,7 +1432,7 @@ int pgl_graph_export_index(const pgl_graph* g, uint64_t* positions, uint32_t* no
         DeviceGuard dg(g->device);
         const uint64_t S = g->sum.total_steps;
         std::vector<StepRec> recs(S);
-        if (S) PGL_CUDA(cudaMemcpy(recs.data(), g->step.p, S * sizeof(StepRec), cudaMemcpyDeviceToHost));
+        if (S) PGL_CUDA(copy_sync(recs.data(), g->step.p, S * sizeof(StepRec), cudaMemcpyDeviceToHost));
         for (uint64_t k = 0; k < S; ++k) {
             const StepRec& r = recs[k];
             if (positions) {
@@ -1388,7 +1441,7 @@ int pgl_graph_export_index(const pgl_graph* g, uint64_t* positions, uint32_t* no
             }
             if (nodes) nodes[k] = r.node;
         }
-        if (cum) PGL_CUDA(cudaMemcpy(cum, g->cum.p, (g->n_paths + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (cum) PGL_CUDA(copy_sync(cum, g->cum.p, (g->n_paths + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_runtime_api.h>
 #include <vector_types.h>
 #include <stdexcept>
 #include <string>
@@ -20,6 +21,19 @@ struct Failure : std::runtime_error {
 
 [[noreturn]] void raise(int type, const std::string& detail);
 [[noreturn]] void raise_cuda(int err, const char* what, const char* file, int line);
+
+// Host <-> device copies go through these so the library can report the
+// bytes it moved (pgl_transfer_bytes: the e2e bench counts them, it does not
+// estimate them).
+void count_copy(cudaMemcpyKind kind, size_t bytes);
+inline cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind kind, cudaStream_t s) {
+    count_copy(kind, n);
+    return cudaMemcpyAsync(dst, src, n, kind, s);
+}
+inline cudaError_t copy_sync(void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
+    count_copy(kind, n);
+    return cudaMemcpy(dst, src, n, kind);
+}
 
 #define PGL_CUDA(call)                                                         \
     do {                                                                       \
@@ -102,7 +116,15 @@ struct IterArgs {
     uint64_t zdef_tab;    //   offset: read speculatively by k_sgd_tiles' cooling units
     const uint4* fguide;  // path guide with inline constants (S < 2^30), see graph_layout
     uint32_t fguide_shift;
+    uint64_t q_off;       // per-iteration start offset of the enumeration: step i = (q + q_off) mod S,
+                          //   so the N mod S extra visits of a pass rotate over the steps
+    // sampler diagnostics (pgl_layout_diag), null when off
+    unsigned int* visits;            // [S] primary visit counts
+    unsigned long long* zhist;       // [zhist_len] Zipf hops drawn
+    unsigned long long* outcomes;    // [4] {uniform attempted, applied, cooling attempted, applied}
+    uint32_t zhist_len;
 };
+
 
 // Device RNG states, structure of arrays (coalesced): s[k][lane].
 struct DevRng {
@@ -112,7 +134,11 @@ struct DevRng {
     uint64_t* s3;
 };
 
-// Accumulated on device with warp-aggregated atomics; RunStats order.
+// Accumulated on device with warp-aggregated atomics; RunStats order:
+// [0] primary steps that reached the update stage, [1] attempted (drf per
+// primary step, engine.cpp:125-126), [2] applied, [3] skipped (counted where
+// each skip happens: an invalid selection skips drf, a d_ref <= 0 update 1),
+// [4..7] batch counters.
 struct DevStats {
     unsigned long long v[8];
 };

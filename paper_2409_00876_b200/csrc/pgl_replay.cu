@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __rest
             ++q;
         }
     } else if (threadIdx.x == 32) {  // ---------------- consumer ----------------
-        unsigned long long applied = 0, bf = 0, bfc = 0, bs = 0;
+        unsigned long long applied = 0, bf = 0, bfc = 0, bs = 0, primary = 0, skipped = 0;
         uint32_t epoch = 0;
         Xo r{rng4[0], rng4[1], rng4[2], rng4[3]};
         uint64_t q = 0, next_step = 0;
@@ -276,11 +276,15 @@ __global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __rest
                 }
                 Xo live = sl.r_mid;
                 bool jitter = false;
+                ++primary;
+                if (!(fl & 1u)) skipped += a.drf;  // engine.cpp:128-131
                 if (fl & 1u) {
                     const StepRec ri = sl.ri, rj = sl.rj;
                     const int ei = (fl >> 3) & 1, ej = (fl >> 4) & 1;
-                    applied += apply_exact(coords, ri.node, ei, rj.node, ej,
-                                           abs_diff(step_pos(ri, ei), step_pos(rj, ej)), a.eta, live, jitter);
+                    const uint32_t ok0 = apply_exact(coords, ri.node, ei, rj.node, ej,
+                                                     abs_diff(step_pos(ri, ei), step_pos(rj, ej)), a.eta, live, jitter);
+                    applied += ok0;
+                    skipped += 1u - ok0;
                     if (a.drf > 1) {
                         unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
                         for (uint32_t extra = 1; extra < a.drf; ++extra) {
@@ -290,8 +294,11 @@ __global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __rest
                                 eb = live.coin() ? 0 : 1;
                             } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
                             used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                            applied += apply_exact(coords, ri.node, ea, rj.node, eb,
-                                                   abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, live, jitter);
+                            const uint32_t ok = apply_exact(coords, ri.node, ea, rj.node, eb,
+                                                            abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, live,
+                                                            jitter);
+                            applied += ok;
+                            skipped += 1u - ok;
                         }
                     }
                 }
@@ -321,7 +328,10 @@ __global__ void __launch_bounds__(64) k_sgd_replay_pc(DevGraph g, double* __rest
         rng4[1] = r.b;
         rng4[2] = r.c;
         rng4[3] = r.d;
+        stats->v[0] += primary;
+        stats->v[1] += primary * a.drf;
         stats->v[2] += applied;
+        stats->v[3] += skipped;
         stats->v[4] += bf;
         stats->v[5] += bfc;
         stats->v[6] += bs;

@@ -41,7 +41,7 @@ __device__ __forceinline__ void flush_stats(DevStats* st, int idx, uint32_t v) {
 // One selected step pair in flight between the two pipeline stages.
 struct Sel {
     StepRec ri, rj;
-    uint32_t flags;  // bit0 valid, bit1 e_i is end, bit2 e_j is end
+    uint32_t flags;  // bit0 valid, bit1 e_i is end, bit2 e_j is end, bit4 active primary step, bit5 cooling
 };
 
 // Stage A (warp-uniform call): the batch decision of engine.cpp:115-124 for
@@ -74,6 +74,7 @@ __device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const Iter
     out.flags = 0;
     out.ri = out.rj = StepRec{0, 0, 0, 0};
     if (!active) return out;
+    out.flags = 16u | (cooling ? 32u : 0u);
     const uint64_t x = r.next();
     const uint64_t pick = __umul64hi(x, g.total_steps);
     const uint32_t p = select_path(g, x, pick);
@@ -81,12 +82,14 @@ __device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const Iter
     const int64_t n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
     if (n < 2) return out;
     const int64_t i = static_cast<int64_t>(pick - pbase);
+    if (a.visits != nullptr) atomicAdd(a.visits + pick, 1u);  // diagnostics only
     int64_t j;
     uint64_t bits;
     if (cooling) {
         const uint32_t zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
         const uint64_t zt = __ldg(&g.pc[p].ztab);
         const int64_t k = static_cast<int64_t>(zipf_alias(g.zalias + zt, zn, r.next()));
+        diag_zipf(a, static_cast<uint64_t>(k));
         bits = r.next();
         const int64_t sign = (bits >> 61) & 1 ? 1 : -1;
         j = i + sign * k;
@@ -109,18 +112,27 @@ __device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const Iter
     out.ri = load_step_stream(g.step + pbase + i, pol_stream);
     out.rj = load_step_stream(g.step + pbase + j, pol_stream);
     // coin true -> Endpoint::start (engine.cpp:89-91): a set bit means start
-    out.flags = 1u | ((bits >> 63) ? 0u : 2u) | (((bits >> 62) & 1) ? 0u : 4u);
+    out.flags = 17u | (cooling ? 32u : 0u) | ((bits >> 63) ? 0u : 2u) | (((bits >> 62) & 1) ? 0u : 4u);
     return out;
 }
 
 // Stage B: the update(s) of one selected pair (engine.cpp:133-170).
 template <typename T>
 __device__ __forceinline__ uint32_t stage_update(const Sel& sel, void* coords, Xo& r, const IterArgs& a,
-                                                 uint64_t pol) {
-    if (!(sel.flags & 1u)) return 0;
+                                                 uint64_t pol, uint32_t& primary, uint32_t& skipped) {
+    if (sel.flags & 16u) ++primary;
+    if (!(sel.flags & 1u)) {
+        if (sel.flags & 16u) {
+            skipped += a.drf;  // an invalid selection skips all drf updates
+            diag_outcome(a, sel.flags & 32u, false);
+        }
+        return 0;
+    }
     const int ei = (sel.flags >> 1) & 1, ej = (sel.flags >> 2) & 1;
     uint32_t applied = hog_update_t<T>(coords, sel.ri.node, ei, sel.rj.node, ej,
                                      abs_diff(step_pos(sel.ri, ei), step_pos(sel.rj, ej)), a.eta, r, pol);
+    skipped += 1u - applied;
+    diag_outcome(a, sel.flags & 32u, applied != 0);
     if (a.drf > 1) {
         unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
         for (uint32_t extra = 1; extra < a.drf; ++extra) {
@@ -131,8 +143,10 @@ __device__ __forceinline__ uint32_t stage_update(const Sel& sel, void* coords, X
                 eb = ((bits >> 62) & 1) ? 0 : 1;
             } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
             used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-            applied += hog_update_t<T>(coords, sel.ri.node, ea, sel.rj.node, eb,
-                                     abs_diff(step_pos(sel.ri, ea), step_pos(sel.rj, eb)), a.eta, r, pol);
+            const uint32_t ok = hog_update_t<T>(coords, sel.ri.node, ea, sel.rj.node, eb,
+                                                abs_diff(step_pos(sel.ri, ea), step_pos(sel.rj, eb)), a.eta, r, pol);
+            applied += ok;
+            skipped += 1u - ok;
         }
     }
     return applied;
@@ -152,7 +166,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, voi
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
 
-    uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
+    uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0, primary = 0, skipped = 0;
     bool carry = false;
     // Two-stage software pipeline over rounds: the step records of round
     // r+1 are in flight while round r gathers and updates coordinates.
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, voi
         if (base + 32 < count)
             nxt = stage_select<true>(g, r, a, base + 32, count, lane, carry, b_first, b_first_cool, b_second,
                                      pol_stream);
-        applied += stage_update<T>(cur, coords, r, a, pol_keep);
+        applied += stage_update<T>(cur, coords, r, a, pol_keep, primary, skipped);
         cur = nxt;
     }
 
@@ -171,7 +185,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, voi
     rng.s1[tid] = r.b;
     rng.s2[tid] = r.c;
     rng.s3[tid] = r.d;
+    flush_stats(stats, 0, primary);
+    flush_stats(stats, 1, primary * a.drf);  // attempted: drf per primary step (engine.cpp:126)
     flush_stats(stats, 2, applied);
+    flush_stats(stats, 3, skipped);
     flush_stats(stats, 4, b_first);
     flush_stats(stats, 5, b_first_cool);
     flush_stats(stats, 6, b_second);

@@ -191,8 +191,8 @@ void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64 /* pgl
     PGL_CUDA(cudaEventRecord(e1, s));
     unsigned long long cnt[2];
     double scal[4];
-    PGL_CUDA(cudaMemcpyAsync(cnt, sc.cnt, sizeof cnt, cudaMemcpyDeviceToHost, s));
-    PGL_CUDA(cudaMemcpyAsync(scal, sc.scal, sizeof scal, cudaMemcpyDeviceToHost, s));
+    PGL_CUDA(copy_async(cnt, sc.cnt, sizeof cnt, cudaMemcpyDeviceToHost, s));
+    PGL_CUDA(copy_async(scal, sc.scal, sizeof scal, cudaMemcpyDeviceToHost, s));
     PGL_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;
     PGL_CUDA(cudaEventElapsedTime(&ms, e0, e1));

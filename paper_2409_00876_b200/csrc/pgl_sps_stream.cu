@@ -377,12 +377,12 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64, uint64
     cudaStream_t s = static_cast<cudaStream_t>(stream_);
     const uint32_t P = g.n_paths;
     std::vector<uint64_t> cum(P + 1);
-    PGL_CUDA(cudaMemcpyAsync(cum.data(), g.cum, (P + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    PGL_CUDA(copy_async(cum.data(), g.cum, (P + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     PGL_CUDA(cudaStreamSynchronize(s));
     static const std::vector<uint64_t> J = jump_tables();
     uint64_t* dj = nullptr;
     PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dj), J.size() * sizeof(uint64_t), s));
-    PGL_CUDA(cudaMemcpyAsync(dj, J.data(), J.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    PGL_CUDA(copy_async(dj, J.data(), J.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
 
     cudaEvent_t e0, e1;
     PGL_CUDA(cudaEventCreate(&e0));
@@ -425,7 +425,7 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64, uint64
         PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scal), 4 * sizeof(double), s));
         PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 2 * sizeof(unsigned long long), s));
         PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&incomplete), sizeof(unsigned), s));
-        PGL_CUDA(cudaMemcpyAsync(dpi, pinfo.data(), P * sizeof(PathInfo), cudaMemcpyHostToDevice, s));
+        PGL_CUDA(copy_async(dpi, pinfo.data(), P * sizeof(PathInfo), cudaMemcpyHostToDevice, s));
         PGL_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), s));
         PGL_CUDA(cudaMemsetAsync(scal, 0, 4 * sizeof(double), s));
         PGL_CUDA(cudaMemsetAsync(incomplete, 0, sizeof(unsigned), s));
@@ -435,7 +435,7 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64, uint64
         k_stream_scan<<<(P + 63) / 64, 64, 0, s>>>(g, seed, dpi, P, dj, maps, prev3, ent, incomplete);
         PGL_CUDA(cudaGetLastError());
         unsigned inc = 0;
-        PGL_CUDA(cudaMemcpyAsync(&inc, incomplete, sizeof inc, cudaMemcpyDeviceToHost, s));
+        PGL_CUDA(copy_async(&inc, incomplete, sizeof inc, cudaMemcpyDeviceToHost, s));
         PGL_CUDA(cudaStreamSynchronize(s));
         if (inc == 0) {
             for (int pass = 0; pass < 2; ++pass) {
@@ -452,8 +452,8 @@ void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64, uint64
                 k_stream_fold<<<1, kFold, 0, s>>>(part, total, pass, cnt, scal);
                 PGL_CUDA(cudaGetLastError());
             }
-            PGL_CUDA(cudaMemcpyAsync(cnt_h, cnt, sizeof cnt_h, cudaMemcpyDeviceToHost, s));
-            PGL_CUDA(cudaMemcpyAsync(scal_h, scal, sizeof scal_h, cudaMemcpyDeviceToHost, s));
+            PGL_CUDA(copy_async(cnt_h, cnt, sizeof cnt_h, cudaMemcpyDeviceToHost, s));
+            PGL_CUDA(copy_async(scal_h, scal, sizeof scal_h, cudaMemcpyDeviceToHost, s));
         }
         PGL_CUDA(cudaStreamSynchronize(s));
         for (void* ptr : {static_cast<void*>(prev3), static_cast<void*>(dpi), static_cast<void*>(maps), static_cast<void*>(ent),

@@ -100,9 +100,14 @@ __device__ __forceinline__ uint32_t path_of_step_fat(const DevGraph& g, const It
         base = static_cast<UX>(e.x);
         n = static_cast<UX>(e.y);
         zdef = (e.z >> 30) & 1u;
-        if (want_z && !zdef) {
-            zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
-            zt = __ldg(&g.pc[p].ztab);
+        if (want_z) {
+            if (zdef) {  // the speculated support: its constants are the kernel's own arguments
+                zn = a.zdef_n;
+                zt = a.zdef_tab;
+            } else {
+                zn = static_cast<uint32_t>(__ldg(&g.pc[p].zn));
+                zt = __ldg(&g.pc[p].ztab);
+            }
         }
         return p;
     }
@@ -141,7 +146,8 @@ __host__ __device__ constexpr size_t async_smem_bytes(int L, bool anchored) {
 struct TileSel {
     StepRec ri, rj;       // rj valid when !(flags & 8)
     uint32_t src;         // lane holding j's record when in-tile
-    uint32_t flags;       // bit0 valid, bit1 e_i end, bit2 e_j end, bit3 j in tile
+    uint32_t flags;       // bit0 valid, bit1 e_i end, bit2 e_j end, bit3 j in tile, bit4 active primary step,
+                          // bit5 cooling
     uint32_t path;        // path of i (warp-shuffle reuse pairs only within a path)
 };
 
@@ -192,6 +198,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     UX u = warp < U ? static_cast<UX>((a.perm_a * static_cast<uint64_t>(warp) + a.perm_b) % a.units) : 0;
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0;
+    // RunStats counted where they happen (engine.cpp:125-126, :128-131, :140-143): primary steps
+    // that reached the update stage, and skipped updates at each skip
+    uint32_t primary = 0, skipped = 0;
     bool carry = false;
     uint32_t b0 = 0;  // this warp's step count mod batch (batch boundaries, engine.cpp:115-124)
 
@@ -268,6 +277,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const UX i0 = unit_i0;                 // first step of the unit, q0 mod S (warp-uniform)
         UX gi = i0 + lane;
         while (gi >= S) gi -= S;               // the unit wraps at the end of a pass (S < 32: repeatedly)
+        if (a.visits != nullptr && active) atomicAdd(a.visits + gi, 1u);  // diagnostics only
+        o.flags = (active ? 16u : 0u) | (cooling ? 32u : 0u);
         // The group leaders draw before the path lookup (a draw that turns
         // out unused is simply discarded), so that in a cooling unit every
         // lane can start the alias-table read for the most common Zipf
@@ -332,6 +343,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             const SX k = static_cast<SX>(
                 shared ? (zdef ? kspec : zipf_alias(g.zalias + zt, zn, draw))
                        : zipf_alias(g.zalias + zt, zn, r.next()));
+            if (!shared || hop_lead) diag_zipf(a, static_cast<uint64_t>(k));  // one count per draw
             const SX sign = (shared ? (tag >> 31) : ((coins >> 1) & 1u)) ? 1 : -1;
             j = i + sign * k;
             if (j < 0 || j >= n) {
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
             else
                 o.rj = load_step_stream(g.step + gj, pol_stream);
         }
-        o.flags = fl;
+        o.flags = fl | 16u | (cooling ? 32u : 0u);
         o.path = p;
         return o;
     };
@@ -418,6 +430,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         const bool live = valid && d_ref > 0.0;
         double vix = 0, viy = 0, vjx = 0, vjy = 0;
         uint32_t got = 0;
+        if (o.flags & 16u) {
+            ++primary;
+            skipped += valid ? (live ? 0u : 1u) : a.drf;  // an invalid selection skips all drf updates
+            diag_outcome(a, o.flags & 32u, live);
+        }
         if (live) {
             CoordHint<T>::get(coords, o.ri.node, ei, pol_keep, vix, viy);
             CoordHint<T>::get(coords, rj.node, ej, pol_keep, vjx, vjy);
@@ -425,8 +442,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         }
         if (a.drf > 1) {
             if (a.reuse_shuffle) {
-                got += shuffle_reuse(live, o.path, o.ri, ei, o.ri.node, vix, viy, step_pos(rj, ej), ej, rj.node, vjx,
-                                     vjy);
+                const uint32_t ex = shuffle_reuse(live, o.path, o.ri, ei, o.ri.node, vix, viy, step_pos(rj, ej), ej,
+                                                  rj.node, vjx, vjy);
+                got += ex;
+                if (valid) skipped += a.drf - 1 - ex;
             } else if (valid) {
                 unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
                 for (uint32_t extra = 1; extra < a.drf; ++extra) {
@@ -437,8 +456,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                         eb = ((b2 >> 62) & 1) ? 0 : 1;
                     } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
                     used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                    got += hog_update_t<T>(coords, o.ri.node, ea, rj.node, eb,
-                                           abs_diff(step_pos(o.ri, ea), step_pos(rj, eb)), a.eta, r, pol_keep);
+                    const uint32_t ok = hog_update_t<T>(coords, o.ri.node, ea, rj.node, eb,
+                                                        abs_diff(step_pos(o.ri, ea), step_pos(rj, eb)), a.eta, r,
+                                                        pol_keep);
+                    got += ok;
+                    skipped += 1u - ok;
                 }
             }
         }
@@ -447,7 +469,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 
     // i0 = 32u mod S, kept incrementally in spread order (no 64-bit division
     // per round): u advances by perm_step, or by perm_step - U on a wrap
-    UX i0 = static_cast<UX>((static_cast<uint64_t>(u) * 32) % g.total_steps);
+    UX i0 = static_cast<UX>((static_cast<uint64_t>(u) * 32 + a.q_off) % g.total_steps);
     const UX perm_step = static_cast<UX>(a.perm_step), i0_step = static_cast<UX>(a.i0_step),
              i0_wrap = static_cast<UX>(a.i0_wrap);
     auto advance = [&](UX& uu, UX& ii) {  // no overflow: uu, perm_step < U < 2^31; ii, i0_* < S < 2^31
@@ -517,6 +539,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 const int cs = wrap(tt_c + (kCS - (2 * L) % kCS) % kCS, kCS), rs = wrap(sel_r + 1, kRS);
                 const AsyncRes cur = s_res[cs][wib][lane];
                 const bool live = (cur.flags & 1u) && cur.d_ref > 0.0;
+                if (cur.flags & 16u) {
+                    ++primary;
+                    skipped += (cur.flags & 1u) ? (live ? 0u : 1u) : a.drf;
+                    diag_outcome(a, cur.flags & 32u, live);
+                }
                 double vix = 0, viy = 0, vjx = 0, vjy = 0;
                 if (live) {
                     if constexpr (kAnch) {
@@ -539,8 +566,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                     const StepRec rj = (cur.flags & 8u) ? s_ri[rs][wib][(cur.flags >> 8) & 31] : s_rj[rs][wib][lane];
                     const int ei = (cur.flags >> 1) & 1, ej = (cur.flags >> 2) & 1;
                     if (a.reuse_shuffle) {
-                        applied += shuffle_reuse(live, cur.flags >> 13, ri, ei, cur.ni, vix, viy, step_pos(rj, ej), ej,
-                                                 cur.nj, vjx, vjy);
+                        const uint32_t ex = shuffle_reuse(live, cur.flags >> 13, ri, ei, cur.ni, vix, viy,
+                                                          step_pos(rj, ej), ej, cur.nj, vjx, vjy);
+                        applied += ex;
+                        if (cur.flags & 1u) skipped += a.drf - 1 - ex;
                     } else if (cur.flags & 1u) {
                         unsigned used = 1u << ((ei ? 2 : 0) | (ej ? 1 : 0));
                         for (uint32_t extra = 1; extra < a.drf; ++extra) {
@@ -551,9 +580,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                                 eb = ((b2 >> 62) & 1) ? 0 : 1;
                             } while (used & (1u << ((ea ? 2 : 0) | (eb ? 1 : 0))));
                             used |= 1u << ((ea ? 2 : 0) | (eb ? 1 : 0));
-                            applied += hog_update_t<T>(coords, ri.node, ea, rj.node, eb,
-                                                       abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta, r,
-                                                       pol_keep);
+                            const uint32_t ok = hog_update_t<T>(coords, ri.node, ea, rj.node, eb,
+                                                                abs_diff(step_pos(ri, ea), step_pos(rj, eb)), a.eta,
+                                                                r, pol_keep);
+                            applied += ok;
+                            skipped += 1u - ok;
                         }
                     }
                 }
@@ -563,7 +594,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
                 __syncwarp();  // in-tile partners read other lanes' copies
                 const int cs = wrap(tt_c + (kCS - L % kCS) % kCS, kCS), rs = wrap(sel_r + L + 1, kRS);
                 const uint32_t fs = s_fl[rs][wib][lane];
-                AsyncRes res{0, 0, 0, 0, 0.0};
+                AsyncRes res{0, 0, fs & 48u, 0, 0.0};  // bits 4-5: active primary step, cooling
                 if (fs & 1u) {
                     const StepRec ri = s_ri[rs][wib][lane];
                     const StepRec rj = (fs & 8u) ? s_ri[rs][wib][(fs >> 8) & 31] : s_rj[rs][wib][lane];
@@ -610,7 +641,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
         rng.s2[tid] = r.c;
         rng.s3[tid] = r.d;
     }
+    flush_stat(stats, 0, primary);
+    flush_stat(stats, 1, primary * a.drf);  // attempted: drf per primary step (engine.cpp:126)
     flush_stat(stats, 2, applied);
+    flush_stat(stats, 3, skipped);
     flush_stat(stats, 4, b_first);
     flush_stat(stats, 5, b_first_cool);
     flush_stat(stats, 6, b_second);
