@@ -303,9 +303,10 @@ def run_ours(args, dist: Dist):
     gen_s = time.perf_counter() - t_gen
     S = g.total_steps()
     cfg = P.LayoutConfig(global_seed=42 + dist.rank, **CONFIG_LAYOUT.get(args.config, {}))
-    if args.coord == "auto":  # the library default: FP64 while it fits L2, anchored FP32 beyond
-        args.coord = "f64" if 32 * g.n_nodes <= (64 << 20) else "anch"
-    coord_kind = {"f64": P.COORD_F64, "f32": P.COORD_F32, "anch": P.COORD_F32_ANCHORED}[args.coord]
+    # auto = the library default (PGL_COORD_AUTO): FP64 while it fits L2,
+    # anchored FP32 beyond when node ids follow path order
+    coord_kind = {"auto": P.COORD_AUTO, "f64": P.COORD_F64, "f32": P.COORD_F32,
+                  "anch": P.COORD_F32_ANCHORED}[args.coord]
     ext = P.LayoutExt(coord_precision=coord_kind)
     updates = cfg.n_iters * (10 * S // cfg.srf) * cfg.drf
 
@@ -313,6 +314,7 @@ def run_ours(args, dist: Dist):
     for _ in range(args.warmup):
         dg.layout(cfg, ext=ext, copy_out=False)
     torch.cuda.synchronize()
+    args.coord = {P.COORD_F64: "f64", P.COORD_F32: "f32", P.COORD_F32_ANCHORED: "anch"}[dg.timing().coord_kind]
 
     clocks = Clocks(dev)
     clocks.start()

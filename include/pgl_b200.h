@@ -322,11 +322,22 @@ typedef struct pgl_timing {
     uint32_t launches;     /* SGD kernel launches (one per iteration) */
     uint32_t grid_blocks;
     uint32_t block_threads;
-    uint32_t _pad0;
+    uint32_t nonfinite_nodes; /* Layout::all_finite on the device after the layout (layout.cpp:9-18):
+                                 nodes with a non-finite coordinate; nonzero raises
+                                 NonFiniteCoordinate */
     uint64_t device_threads; /* resident lanes = concurrent Hogwild workers*32 */
+    uint32_t coord_kind;      /* pgl_coord_precision the layout ran with (PGL_COORD_AUTO resolved) */
+    uint32_t _pad1;
 } pgl_timing;
 
 int pgl_graph_last_timing(const pgl_graph* g, pgl_timing* out);
+
+/* Layout::all_finite (layout.cpp:9-18) on the device: how many nodes have a
+ * non-finite coordinate, and the first such node id (0 if none), for the
+ * resident layout (coords NULL) or a host layout [4*n_nodes]. Every layout
+ * call runs the same check on its result and raises NonFiniteCoordinate
+ * when it fails. */
+int pgl_graph_all_finite(pgl_graph* g, const double* coords, uint64_t* bad_nodes, uint64_t* first_bad);
 
 /* ---- sampled path stress: the drop-in for sampled_path_stress ----------- */
 

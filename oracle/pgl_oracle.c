@@ -604,17 +604,20 @@ void orc_exact_path_stress(const orc_graph* g, const double* c, pgl_stress_repor
 }
 
 /* ---- the product's counter-based SPS estimator, restated ---------------- */
-/* Sample space: flat index q in [spn*cum[p], spn*cum[p+1]) for path p with
- * >= 2 steps; local index s = q - spn*cum[p]. Draw t of sample s is the
- * splitmix64 output at counter s*64 + t of a stream keyed by
- * splitmix64(seed ^ phi*(2^61 + p + 1)). i, j distinct uniform (j redrawn
- * with counters 1..47), then up to 9 coin attempts at counters 48..56 (top
- * bit -> e_i, next bit -> e_j, set -> start). Fixed-order reduction: chunks
- * of SPS_CHUNK flat samples; within a chunk lane l (of SPS_LANES) adds
- * samples l, l+SPS_LANES, ... in order, then a halving tree; chunk partials
- * are folded by SPS_FINAL lanes with stride SPS_FINAL, then a halving tree. */
+/* (pgl_sps.cu, PGL_SPS_COUNTER.) Path p with ns = |p| >= 2 steps has
+ * spn*ns samples; sample s takes the primary step i = s mod ns (each step
+ * exactly spn times) and j uniform over the other ns-1 steps:
+ * j = hi64(draw(s*16) * (ns-1)), +1 when j >= i. Draw t of sample s is the
+ * splitmix64 output at counter s*16 + t of the stream keyed by
+ * splitmix64(seed ^ phi*(2^61 + p + 1)); up to 9 coin attempts at counters
+ * s*16+1 .. s*16+9 (top bit -> e_i, next bit -> e_j, set -> start) for a
+ * nonzero d_ref (metrics.cpp:116-148). Reduction, in this exact order:
+ * path-major chunks of SPS_CHUNK samples; in a chunk lane l (of SPS_LANES)
+ * runs Welford over samples l, l+SPS_LANES, ...; lane moments are merged by
+ * a halving tree (Chan et al. pairwise merge); chunk moments are folded by
+ * SPS_FINAL lanes with stride SPS_FINAL, then a halving tree. */
 #define SPS_LANES 256
-#define SPS_CHUNK 4096
+#define SPS_CHUNK 16384
 #define SPS_FINAL 1024
 
 static inline uint64_t ctr_draw(uint64_t key, uint64_t ctr) {
@@ -629,28 +632,13 @@ static inline uint64_t ctr_key(uint64_t seed, uint32_t p) {
     return splitmix_step(&key);
 }
 
-/* returns 1 term, 0 skipped, -1 no sample (path with < 2 steps) */
-static int ctr_sample(const orc_graph* g, const double* c, uint64_t seed, uint32_t spn, uint64_t q,
-                      double* term) {
-    /* path of flat sample q: largest p with spn*cum[p] <= q */
-    uint32_t lo = 0, hi = g->n_paths;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) / 2;
-        if ((uint64_t)spn * g->cum[mid] <= q) lo = mid;
-        else hi = mid;
-    }
-    const uint32_t p = lo;
-    const uint64_t ns = g->cum[p + 1] - g->cum[p], base = g->cum[p];
-    if (ns < 2) return -1;
-    const uint64_t s = q - (uint64_t)spn * g->cum[p];
-    const uint64_t key = ctr_key(seed, p);
-    const uint64_t i = (uint64_t)(((unsigned __int128)ctr_draw(key, s * 64) * ns) >> 64);
-    uint64_t j = i;
-    for (uint64_t t = 1; t < 48 && j == i; ++t)
-        j = (uint64_t)(((unsigned __int128)ctr_draw(key, s * 64 + t) * ns) >> 64);
-    if (j == i) return 0;
+/* returns 1 with a term, 0 skipped (9 degenerate coin pairs) */
+static int ctr_sample(const orc_graph* g, const double* c, uint64_t key, uint64_t base, uint64_t ns, uint64_t s,
+                      uint64_t i, double* term) {
+    uint64_t j = (uint64_t)(((unsigned __int128)ctr_draw(key, s * 16) * (ns - 1)) >> 64);
+    if (j >= i) ++j;
     for (uint64_t a = 0; a < 9; ++a) {
-        const uint64_t r = ctr_draw(key, s * 64 + 48 + a);
+        const uint64_t r = ctr_draw(key, s * 16 + 1 + a);
         const int ei = (r >> 63) ? 0 : 1, ej = ((r >> 62) & 1) ? 0 : 1;
         const uint64_t pi = position(g, base + i, ei), pj = position(g, base + j, ej);
         if (pi == pj) continue;
@@ -662,9 +650,27 @@ static int ctr_sample(const orc_graph* g, const double* c, uint64_t seed, uint32
     return 0;
 }
 
-static double tree(double* v, int n) {
+typedef struct { double n, mean, m2; } moments;
+
+static inline void mpush(moments* a, double t) {
+    a->n += 1.0;
+    const double d = t - a->mean;
+    a->mean += d / a->n;
+    a->m2 += d * (t - a->mean);
+}
+
+static inline moments mmerge(moments a, moments b) {
+    if (b.n == 0.0) return a;
+    if (a.n == 0.0) return b;
+    const double n = a.n + b.n;
+    const double d = b.mean - a.mean;
+    moments r = {n, a.mean + d * (b.n / n), a.m2 + b.m2 + d * d * (a.n * b.n / n)};
+    return r;
+}
+
+static moments mtree(moments* v, int n) {
     for (int stride = n / 2; stride >= 1; stride /= 2)
-        for (int k = 0; k < stride; ++k) v[k] += v[k + stride];
+        for (int k = 0; k < stride; ++k) v[k] = mmerge(v[k], v[k + stride]);
     return v[0];
 }
 
@@ -672,42 +678,42 @@ int orc_sps_counter(const orc_graph* g, const double* c, uint64_t seed, uint32_t
                     pgl_stress_report* r) {
     if (spn < 1) return fail(PGL_ERR_INVALID_PARAMETER, "InvalidParameter", "samples_per_node must be >= 1");
     memset(r, 0, sizeof *r);
-    const uint64_t Q = (uint64_t)spn * g->total_steps;
-    const uint64_t n_chunks = (Q + SPS_CHUNK - 1) / SPS_CHUNK;
-    double* part = (double*)calloc(n_chunks + 1, sizeof(double));
-    double lane[SPS_LANES], fin[SPS_FINAL];
-    double mean = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-        for (uint64_t ch = 0; ch < n_chunks; ++ch) {
+    uint64_t n_chunks = 0;
+    for (uint32_t p = 0; p < g->n_paths; ++p) {
+        const uint64_t ns = g->cum[p + 1] - g->cum[p];
+        if (ns >= 2) n_chunks += ((uint64_t)spn * ns + SPS_CHUNK - 1) / SPS_CHUNK;
+    }
+    moments* part = (moments*)calloc(n_chunks + 1, sizeof(moments));
+    moments lane[SPS_LANES], fin[SPS_FINAL];
+    uint64_t ch = 0;
+    for (uint32_t p = 0; p < g->n_paths; ++p) {
+        const uint64_t base = g->cum[p], ns = g->cum[p + 1] - base;
+        if (ns < 2) continue;
+        const uint64_t key = ctr_key(seed, p), q = (uint64_t)spn * ns;
+        for (uint64_t s0 = 0; s0 < q; s0 += SPS_CHUNK, ++ch) {
             for (int l = 0; l < SPS_LANES; ++l) {
-                double acc = 0.0;
-                for (uint64_t q = ch * SPS_CHUNK + l; q < (ch + 1) * SPS_CHUNK && q < Q; q += SPS_LANES) {
+                moments m = {0.0, 0.0, 0.0};
+                for (uint64_t s = s0 + (uint64_t)l; s < s0 + SPS_CHUNK && s < q; s += SPS_LANES) {
                     double t;
-                    const int k = ctr_sample(g, c, seed, spn, q, &t);
-                    if (k == 1) {
-                        if (pass == 0) { acc += t; ++r->n; }
-                        else acc += (t - mean) * (t - mean);
-                    } else if (k == 0 && pass == 0) {
+                    if (ctr_sample(g, c, key, base, ns, s, s % ns, &t))
+                        mpush(&m, t);
+                    else
                         ++r->skipped;
-                    }
                 }
-                lane[l] = acc;
+                lane[l] = m;
             }
-            part[ch] = tree(lane, SPS_LANES);
-        }
-        for (int l = 0; l < SPS_FINAL; ++l) {
-            double acc = 0.0;
-            for (uint64_t ch = (uint64_t)l; ch < n_chunks; ch += SPS_FINAL) acc += part[ch];
-            fin[l] = acc;
-        }
-        const double total = tree(fin, SPS_FINAL);
-        if (pass == 0) {
-            mean = r->n > 0 ? total / (double)r->n : 0.0;
-            r->mean = mean;
-        } else {
-            finish(r, total);
+            part[ch] = mtree(lane, SPS_LANES);
         }
     }
+    for (int l = 0; l < SPS_FINAL; ++l) {
+        moments acc = {0.0, 0.0, 0.0};
+        for (uint64_t k = (uint64_t)l; k < n_chunks; k += SPS_FINAL) acc = mmerge(acc, part[k]);
+        fin[l] = acc;
+    }
+    const moments tot = mtree(fin, SPS_FINAL);
+    r->n = (uint64_t)tot.n;
+    r->mean = tot.mean;
+    finish(r, tot.m2);
     free(part);
     return 0;
 }

@@ -115,7 +115,8 @@ class _Info(C.Structure):
 class _Timing(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("init_ms", C.c_double), ("total_ms", C.c_double),
                 ("device_ms", C.c_double), ("launches", C.c_uint32), ("grid_blocks", C.c_uint32), ("block_threads", C.c_uint32),
-                ("_pad0", C.c_uint32), ("device_threads", C.c_uint64)]
+                ("nonfinite_nodes", C.c_uint32), ("device_threads", C.c_uint64),
+                ("coord_kind", C.c_uint32), ("_pad1", C.c_uint32)]
 
 
 class _GfaInfo(C.Structure):
@@ -136,6 +137,7 @@ _sig = {
     "pgl_last_error": ([], C.c_char_p), "pgl_last_error_type": ([], C.c_int),
     "pgl_abi_version": ([], C.c_int), "pgl_device_count": ([], C.c_int),
     "pgl_transfer_bytes": ([_u64p, _u64p], C.c_int),
+    "pgl_graph_all_finite": ([_vp, _f64p, _u64p, _u64p], C.c_int),
     "pgl_layout_run": ([C.c_int, C.POINTER(_View), C.POINTER(_Cfg), C.POINTER(_Ext), C.c_int, _CB,
                         C.c_int, _vp, _f64p, C.POINTER(_Stats)], C.c_int),
     "pgl_graph_create": ([C.c_int, C.POINTER(_View), C.POINTER(_vp)], C.c_int),
@@ -365,6 +367,8 @@ class Timing:
     grid_blocks: int
     block_threads: int
     device_threads: int
+    nonfinite_nodes: int = 0
+    coord_kind: int = 0
 
 
 # ---- graphs -----------------------------------------------------------------------
@@ -743,7 +747,18 @@ class DeviceGraph:
         t = _Timing()
         _check(_lib.pgl_graph_last_timing(self.h, C.byref(t)))
         return Timing(t.kernel_ms, t.init_ms, t.total_ms, t.device_ms, t.launches, t.grid_blocks, t.block_threads,
-                      t.device_threads)
+                      t.device_threads, t.nonfinite_nodes, t.coord_kind)
+
+    def all_finite(self, layout: Optional[np.ndarray] = None):
+        """Layout::all_finite on the device: (bad node count, first bad node)
+        of the resident layout or of `layout`."""
+        c = None if layout is None else np.ascontiguousarray(layout, np.float64).reshape(-1)
+        if c is not None and c.size != 4 * self.n_nodes:
+            raise CountMismatch("CountMismatch: layout size does not match the graph")
+        bad, first = C.c_uint64(0), C.c_uint64(0)
+        _check(_lib.pgl_graph_all_finite(self.h, c.ctypes.data_as(_f64p) if c is not None else None,
+                                         C.byref(bad), C.byref(first)))
+        return int(bad.value), int(first.value)
 
     def stress(self, seed: int, samples_per_node: int = 100, layout: Optional[np.ndarray] = None,
                method: int = SPS_COUNTER, return_ms: bool = False):

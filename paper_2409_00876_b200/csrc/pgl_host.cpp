@@ -396,6 +396,7 @@ struct pgl_graph {
     DevBuf<double> coords64;             // [4V] FP64 layout / staging
     DevBuf<float> coords32;              // [4V] FP32 layout
     int layout_f64 = -1;                 // precision of the resident layout (-1: none)
+    int ids_local = -1;                  // node ids follow path order (anchored store usable); -1 unknown
     DevBuf<uint64_t> rng;                // SoA xoshiro states
     DevBuf<unsigned long long> stats;    // [8]
     SpsScratch sps{};
@@ -635,7 +636,7 @@ pgl_graph* create_graph(int device, const pgl_graph_view* v) {
     G->node_len.assign(v->node_len, v->node_len + v->n_nodes);
     G->path_n_steps.assign(v->path_n_steps, v->path_n_steps + v->n_paths);
     pack_graph(G.get(), v);
-    G->stats.alloc(8);
+    G->stats.alloc(10);
     return G.release();
 }
 
@@ -688,7 +689,7 @@ pgl_graph* create_graph_gfa(int device, GfaGraph* gf) {
     PGL_CUDA(copy_async(dsteps.p, c.steps, sm.total_steps * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
     build_records_device(dsteps.p, dlen.p, G->cum.p, c.n_paths, sm.total_steps, G->step.p, G->stream);
     PGL_CUDA(cudaStreamSynchronize(G->stream));
-    G->stats.alloc(8);
+    G->stats.alloc(10);
     return G.release();
 }
 
@@ -781,7 +782,26 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     const int replay = ext.mode == PGL_MODE_REPLAY;
     // coordinate store: pgl_coord_precision (replay is FP64)
     int kind = replay ? PGL_COORD_F64 : static_cast<int>(ext.coord_precision);
-    if (kind == PGL_COORD_AUTO) kind = 32 * G->n_nodes <= (64ULL << 20) ? PGL_COORD_F64 : PGL_COORD_F32_ANCHORED;
+    if (kind == PGL_COORD_AUTO) {
+        // FP64 while the array fits comfortably in L2; beyond that the
+        // anchored FP32 store -- which needs blocks of 32 consecutive node ids
+        // to lie close together along the paths (true for build_graph /
+        // write_gfa numbering, not for an arbitrary GFA id order): checked on
+        // the device once per graph, >= 99% of the blocks within 2^20 nt
+        if (32 * G->n_nodes <= (64ULL << 20)) {
+            kind = PGL_COORD_F64;
+        } else {
+            if (G->ids_local < 0) {
+                unsigned long long r[2];
+                block_span_stats(G->step.p, G->sum.total_steps, G->n_nodes, (1u << 20) / 256, G->stats.p + 8,
+                                 G->stream);
+                PGL_CUDA(copy_async(r, G->stats.p + 8, sizeof r, cudaMemcpyDeviceToHost, G->stream));
+                PGL_CUDA(cudaStreamSynchronize(G->stream));
+                G->ids_local = r[0] * 100 <= r[1] ? 1 : 0;
+            }
+            kind = G->ids_local ? PGL_COORD_F32_ANCHORED : PGL_COORD_F64;
+        }
+    }
     const uint64_t V = G->n_nodes;
 
     // init_layout on the host (bit-exact), upload, narrow to FP32 on device.
@@ -888,7 +908,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (!tables.empty())
         PGL_CUDA(copy_async(G->zalias.p, tables.data(), tables.size() * sizeof(ZipfAlias),
                                  cudaMemcpyHostToDevice, G->stream));
-    PGL_CUDA(cudaMemsetAsync(G->stats.p, 0, 8 * sizeof(unsigned long long), G->stream));
+    PGL_CUDA(cudaMemsetAsync(G->stats.p, 0, 10 * sizeof(unsigned long long), G->stream));
 
     // RNG states: lane t <- seed_worker(seed, t) (rng.hpp:63-71)
     LaunchShape shape;
@@ -1030,6 +1050,9 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         }
     }
     PGL_CUDA(cudaEventRecord(ev_end, G->stream));
+    // Layout::all_finite (layout.cpp:9-18) of the result, on the device:
+    // stats[8] = nodes with a non-finite coordinate, stats[9] = the first one
+    launch_count_nonfinite(coords, kind, V, G->stats.p + 8, G->stream);
     PGL_CUDA(cudaStreamSynchronize(G->stream));
     G->layout_f64 = kind;
     {
@@ -1051,8 +1074,14 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (!replay && prev_gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, prev_gran);
     if (aborted) raise(PGL_ERR_CALLBACK, "iteration callback requested abort");
 
-    unsigned long long dst[8];
+    unsigned long long dst[10];
     PGL_CUDA(copy_sync(dst, G->stats.p, sizeof dst, cudaMemcpyDeviceToHost));
+    G->timing.coord_kind = static_cast<uint32_t>(kind);
+    G->timing.nonfinite_nodes = static_cast<uint32_t>(std::min<unsigned long long>(dst[8], 0xFFFFFFFFull));
+    if (dst[8])
+        raise(PGL_ERR_NON_FINITE_COORDINATE, "node " + std::to_string(dst[9]) +
+                                                 " has a non-finite coordinate after the layout (" +
+                                                 std::to_string(dst[8]) + " nodes; device all_finite check)");
     if (stats_out) {
         // every field is a device count (DevStats); tests hold them to the
         // reference's identities (test_engine.cpp:257-278)
@@ -1121,7 +1150,7 @@ void graph_stress(pgl_graph* G, const double* coords, uint64_t seed, uint32_t sp
     }
     std::memset(out, 0, sizeof *out);
     if (method == PGL_SPS_COUNTER)
-        run_sps_counter(G->dev(), dc, f64, seed, spn, G->sps, out, kernel_ms, G->stream);
+        run_sps_counter(G->dev(), dc, f64, G->path_n_steps.data(), seed, spn, G->sps, out, kernel_ms, G->stream);
     else if (method == PGL_SPS_STREAM)
         run_sps_stream(G->dev(), dc, f64, seed, spn, out, kernel_ms, G->stream);
     else
@@ -1488,6 +1517,33 @@ int pgl_graph_stress(pgl_graph* g, const double* coords, uint64_t seed, uint32_t
     return guarded([&] {
         if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
         graph_stress(g, coords, seed, spn, method, out, kernel_ms);
+    });
+}
+
+int pgl_graph_all_finite(pgl_graph* g, const double* coords, uint64_t* bad_nodes, uint64_t* first_bad) {
+    return guarded([&] {
+        if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
+        DeviceGuard dg(g->device);
+        const uint64_t V = g->n_nodes;
+        const void* dc;
+        int kind;
+        if (coords) {
+            g->coords64.alloc(4 * V);
+            PGL_CUDA(copy_async(g->coords64.p, coords, 4 * V * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+            dc = g->coords64.p;
+            kind = PGL_COORD_F64;
+            g->layout_f64 = -1;  // the resident layout is overwritten
+        } else {
+            if (g->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
+            kind = g->layout_f64;
+            dc = kind == PGL_COORD_F64 ? static_cast<const void*>(g->coords64.p) : static_cast<const void*>(g->coords32.p);
+        }
+        launch_count_nonfinite(dc, kind, V, g->stats.p + 8, g->stream);
+        unsigned long long r[2];
+        PGL_CUDA(copy_async(r, g->stats.p + 8, sizeof r, cudaMemcpyDeviceToHost, g->stream));
+        PGL_CUDA(cudaStreamSynchronize(g->stream));
+        if (bad_nodes) *bad_nodes = r[0];
+        if (first_bad) *first_bad = r[0] ? r[1] : 0;
     });
 }
 

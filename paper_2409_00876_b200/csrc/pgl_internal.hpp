@@ -168,14 +168,14 @@ void launch_sgd_replay(const DevGraph& g, double* coords, uint64_t* rng4,
                        DevStats* stats, const IterArgs& a, void* stream);
 
 struct SpsScratch {
-    double* part;            // [n_chunks]
-    unsigned long long* cnt; // [2]: n, skipped
-    double* scal;            // [4]: sum, mean, ssd, spare
-    uint64_t n_chunks_cap;
+    void* part;              // per-chunk moments + chunk prefix per path
+    unsigned long long* cnt; // [2]: spare, skipped
+    double* scal;            // [4]: total moments (n, mean, M2), spare
+    size_t part_bytes;
 };
 // Counter-based sampled path stress on a resident graph (metrics.cpp:108-159
 // estimator). Fills out (mean, n, sd, ci) deterministically.
-void run_sps_counter(const DevGraph& g, const void* coords, int coord_f64,
+void run_sps_counter(const DevGraph& g, const void* coords, int coord_kind, const uint64_t* path_n_steps,
                      uint64_t seed, uint32_t spn, SpsScratch& scratch,
                      pgl_stress_report* out, double* kernel_ms, void* stream);
 void run_sps_stream(const DevGraph& g, const void* coords, int coord_f64,
@@ -223,6 +223,12 @@ void launch_f64_to_f32(const double* src, float* dst, uint64_t n, void* stream);
 void launch_f64_to_anch(const double* src, void* dst, uint64_t n_nodes, void* stream);
 void launch_anch_to_f64(const void* src, double* dst, uint64_t n_nodes, void* stream);
 void launch_reanchor(void* store, uint64_t n_nodes, void* stream);
+// out[0] = blocks of 32 node ids whose path positions span more than
+// max_span_256nt * 256 nt, out[1] = blocks visited by some step
+void block_span_stats(const StepRec* step, uint64_t S, uint64_t n_nodes, uint32_t max_span_256nt,
+                      unsigned long long* out, void* stream);
+void launch_count_nonfinite(const void* coords, int coord_kind, uint64_t n_nodes, unsigned long long* out,
+                            void* stream);
 void launch_f32_to_f64(const float* src, double* dst, uint64_t n, void* stream);
 
 // ---- host helpers (pgl_host.cpp) -----------------------------------------

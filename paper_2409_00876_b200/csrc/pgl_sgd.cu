@@ -14,6 +14,8 @@
 // (PGL_MODE_REPLAY lives in pgl_replay.cu.)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "pgl_device.cuh"
 
 namespace pgl {
@@ -306,6 +308,99 @@ __global__ void k_reanchor(char* __restrict__ store, uint64_t V) {
         __syncwarp();
         if (lane == 0) *reinterpret_cast<double*>(blk) = a_new;
     }
+}
+
+// Id locality of the graph, for the anchored store's auto choice: for each
+// block of 32 consecutive node ids, the range of the path positions
+// (256-nt units) of the steps that visit its nodes; lanes of a warp that hit
+// the same block combine first (__match_any_sync). A block whose nodes lie
+// far apart along the paths would hold f32 offsets far from its anchor.
+__global__ void k_block_span(const StepRec* __restrict__ step, uint64_t S, unsigned int* __restrict__ lo,
+                             unsigned int* __restrict__ hi) {
+    for (uint64_t k0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); k0 < S;
+         k0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t k = k0 + threadIdx.x;
+        const bool ok = k < S;
+        uint32_t blk = 0xFFFFFFFFu, pos = 0;
+        if (ok) {
+            const StepRec r = step[k];
+            blk = r.node >> 5;
+            const uint64_t p = static_cast<uint64_t>(r.ps_lo) | (static_cast<uint64_t>(r.hi & 0xFFFFu) << 32);
+            pos = static_cast<uint32_t>(p >> 8);
+        }
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, blk);
+        const uint32_t mn = __reduce_min_sync(peers, pos), mx = __reduce_max_sync(peers, pos);
+        if (ok && (threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1)) {
+            atomicMin(lo + blk, mn);
+            atomicMax(hi + blk, mx);
+        }
+    }
+}
+
+__global__ void k_count_wide_blocks(const unsigned int* __restrict__ lo, const unsigned int* __restrict__ hi,
+                                    uint64_t n_blocks, uint32_t max_span, unsigned long long* out) {
+    uint32_t wide = 0, seen = 0;
+    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < n_blocks;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (lo[b] <= hi[b]) {
+            ++seen;
+            wide += hi[b] - lo[b] > max_span;
+        }
+    }
+    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, wide), s = __reduce_add_sync(0xFFFFFFFFu, seen);
+    if ((threadIdx.x & 31) == 0) {
+        if (w) atomicAdd(out, static_cast<unsigned long long>(w));
+        if (s) atomicAdd(out + 1, static_cast<unsigned long long>(s));
+    }
+}
+
+void block_span_stats(const StepRec* step, uint64_t S, uint64_t n_nodes, uint32_t max_span_256nt,
+                      unsigned long long* out, void* stream) {
+    auto s = static_cast<cudaStream_t>(stream);
+    const uint64_t nb = (n_nodes + 31) / 32;
+    unsigned int* buf = nullptr;
+    PGL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), 2 * std::max<uint64_t>(nb, 1) * sizeof(unsigned int), s));
+    PGL_CUDA(cudaMemsetAsync(buf, 0xFF, nb * sizeof(unsigned int), s));
+    PGL_CUDA(cudaMemsetAsync(buf + nb, 0, nb * sizeof(unsigned int), s));
+    PGL_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), s));
+    if (S) k_block_span<<<1184, 256, 0, s>>>(step, S, buf, buf + nb);
+    k_count_wide_blocks<<<592, 256, 0, s>>>(buf, buf + nb, nb, max_span_256nt, out);
+    PGL_CUDA(cudaGetLastError());
+    PGL_CUDA(cudaFreeAsync(buf, s));
+}
+
+// Layout::all_finite (layout.cpp:9-18) on the device: count the nodes with
+// a non-finite coordinate and the smallest such node id (out[0], out[1];
+// out[1] starts at ~0).
+template <typename T>
+__global__ void k_count_nonfinite(const void* __restrict__ coords, uint64_t V, unsigned long long* out) {
+    uint32_t bad = 0;
+    for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < V;
+         n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double sx, sy, ex, ey;
+        Coord<T>::get(coords, static_cast<uint32_t>(n), 0, sx, sy);
+        Coord<T>::get(coords, static_cast<uint32_t>(n), 1, ex, ey);
+        if (!(isfinite(sx) && isfinite(sy) && isfinite(ex) && isfinite(ey))) {
+            ++bad;
+            atomicMin(out + 1, static_cast<unsigned long long>(n));
+        }
+    }
+    const uint32_t b = __reduce_add_sync(0xFFFFFFFFu, bad);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, static_cast<unsigned long long>(b));
+}
+
+void launch_count_nonfinite(const void* coords, int coord_kind, uint64_t n_nodes, unsigned long long* out,
+                            void* stream) {
+    auto s = static_cast<cudaStream_t>(stream);
+    PGL_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), s));
+    PGL_CUDA(cudaMemsetAsync(out + 1, 0xFF, sizeof(unsigned long long), s));
+    if (coord_kind == PGL_COORD_F64)
+        k_count_nonfinite<double><<<592, 256, 0, s>>>(coords, n_nodes, out);
+    else if (coord_kind == PGL_COORD_F32)
+        k_count_nonfinite<float><<<592, 256, 0, s>>>(coords, n_nodes, out);
+    else
+        k_count_nonfinite<AnchF32><<<592, 256, 0, s>>>(coords, n_nodes, out);
+    PGL_CUDA(cudaGetLastError());
 }
 
 void launch_reanchor(void* store, uint64_t n_nodes, void* stream) {

@@ -639,3 +639,52 @@ def test_index_from_view_offsets_when_not_prefix_sums(pgl, gpu):
             pos, nodes, _ = dg.export_index()
         assert pos.tolist() == [list(w) for w in want]
         assert nodes.tolist() == [int(st["node_id"]) for a in arrs for st in a]
+
+
+# ---- Layout::all_finite on the device (layout.cpp:9-18) ------------------------------
+
+@pytest.mark.parametrize("prec", [0, 1, 2])
+def test_all_finite_device_check(pgl, gpu, prec):
+    """Every layout call checks its result on the device (a non-finite
+    coordinate raises NonFiniteCoordinate); the same reduction is exposed
+    for any layout."""
+    g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
+    with pgl.DeviceGraph(g) as dg:
+        lay = dg.layout(pgl.LayoutConfig(n_iters=3), ext=pgl.LayoutExt(coord_precision=prec))
+        assert dg.timing().nonfinite_nodes == 0
+        assert dg.all_finite() == (0, 0)
+        bad = lay.copy()
+        bad[4 * 9] = np.inf
+        bad[4 * 7 + 3] = np.nan
+        assert dg.all_finite(bad) == (2, 7)
+        assert dg.all_finite(lay) == (0, 0)
+
+
+def test_auto_store_checks_id_locality(pgl, gpu):
+    """PGL_COORD_AUTO picks the anchored FP32 store beyond 64 MiB of FP64
+    coordinates only when blocks of 32 consecutive node ids lie close along
+    the paths (build_graph / write_gfa numbering); with an arbitrary id order
+    (a GFA from another tool) it stays FP64 instead of losing precision."""
+    g = pgl.generate_synthetic_pangenome(1, 2_100_000, 2, 0.05)
+    assert 32 * g.n_nodes > (64 << 20)
+    cfg = pgl.LayoutConfig(n_iters=30)
+    with pgl.DeviceGraph(g) as dg:
+        dg.layout(cfg, copy_out=False)
+        assert dg.timing().coord_kind == pgl.COORD_F32_ANCHORED
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(g.n_nodes).astype(np.uint32)  # old id -> new id
+    node_len = np.empty_like(g.node_len)
+    node_len[perm] = g.node_len
+    steps = []
+    for p in g.path_steps:
+        q = p.copy()
+        q["node_id"] = perm[p["node_id"]]
+        steps.append(q)
+    h = pgl.PangenomeGraph(node_len, steps)
+    with pgl.DeviceGraph(h) as dg:
+        dg.layout(cfg, copy_out=False)
+        assert dg.timing().coord_kind == pgl.COORD_F64
+        auto = dg.stress(7, 10).mean
+        dg.layout(cfg, ext=pgl.LayoutExt(coord_precision=pgl.COORD_F32_ANCHORED), copy_out=False)
+        forced = dg.stress(7, 10).mean
+    assert auto <= forced
