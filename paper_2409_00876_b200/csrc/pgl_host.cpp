@@ -708,7 +708,10 @@ constexpr uint32_t kHopLanes = 8;  // default lanes per shared Zipf hop
 // pipeline at 3 CTAs/SM once the concurrency cap allows 8 warps per SM,
 // else the register pipeline, whose shorter read-to-write window keeps
 // small graphs' layouts closest to the reference.
-int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
+// lean_ok: the run is one the lean async kernel (variants 7, 8) covers --
+// batch 32, drf 1, no warp-shuffle reuse, the shared window + Zipf-hop
+// sampler, 32 <= S < 2^30 steps, paths shorter than 2^32 nt.
+int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_ok) {
     int v = static_cast<int>(ext.kernel_variant & 15);
     const int force64 = static_cast<int>(ext.kernel_variant & 16);
     if (v == 0) {
@@ -716,13 +719,18 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap) {
         PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         // the async pipeline once the cap allows a CTA's worth of warps per
         // SM (config 5, cap 2988 warps: 38.7 vs 36.1 G upd/s for variant 1,
-        // at lower SPS); the register pipeline's shorter read-to-write window
-        // where the cap binds hard (config 1)
-        v = cap >= static_cast<uint32_t>(sms) * 8 ? 6 : 1;
+        // at lower SPS) -- its lean specialisation where the run allows;
+        // the register pipeline's shorter read-to-write window where the
+        // cap binds hard (config 1)
+        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 7 : 6) : 1;
     }
-    if (v != 1 && v != 2 && v != 5 && v != 6)
-        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5, 6");
-    return v | force64;
+    if (v != 1 && v != 2 && v != 5 && v != 6 && v != 7 && v != 8)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5, 6, 7, 8");
+    if ((v == 7 || v == 8) && (!lean_ok || force64))
+        raise(PGL_ERR_INVALID_PARAMETER,
+              "pgl_layout_ext.kernel_variant 7/8 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
+              "pair_window 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
+    return v | force64 | ((v == 7 || v == 8) && ext.diag ? 32 : 0);
 }
 
 uint32_t auto_max_warps(uint64_t n_nodes) {
@@ -914,12 +922,15 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     LaunchShape shape;
     uint32_t n_warps = 1;
     uint64_t lanes = 1;
+    const bool lean_ok = cfg.batch_size == 32 && cfg.drf == 1 && !ext.reuse_shuffle &&
+                         (ext.pair_window == 0 || ext.pair_window == 3) && G->sum.total_steps >= 32 &&
+                         G->sum.total_steps < (1ULL << 30) && G->sum.max_path_len < (1ULL << 32);
     if (!replay) {
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
         shape = ext.sampling == PGL_SAMPLING_IID
                     ? sgd_shape(G->device, kind, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
                     : tiles_shape(G->device, kind, cap, static_cast<int>(ext.block_threads),
-                                  tile_variant(G->device, ext, cap), G->sum.total_steps);
+                                  tile_variant(G->device, ext, cap, lean_ok), G->sum.total_steps);
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -994,10 +1005,15 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         a.drf = cfg.drf;
         a.n_warps = n_warps;
         a.units = (spi + 31) / 32;
+        const bool lean = !replay && ext.sampling == PGL_SAMPLING_TILES &&
+                          ((shape.variant & 15) == 7 || (shape.variant & 15) == 8);
+        a.units_full = spi / 32;
+        a.tail_n = static_cast<uint32_t>(spi % 32);
         {   // unit order of k_sgd_tiles: u = (a*k + b) mod U, gcd(a, U) = 1,
-            // a near U/phi (low-discrepancy), jittered per iteration
+            // a near U/phi (low-discrepancy), jittered per iteration (the lean
+            // kernel permutes the full units only)
             HostRng pr(cfg.global_seed, (1ULL << 59) + it);
-            const uint64_t U = std::max<uint64_t>(a.units, 1);
+            const uint64_t U = std::max<uint64_t>(lean ? a.units_full : a.units, 1);
             uint64_t m = static_cast<uint64_t>(static_cast<double>(U) * 0.6180339887498949) + pr.below(U / 16 + 1);
             m %= U;
             if (m == 0) m = 1;
@@ -1022,6 +1038,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             // rotate the enumeration's start every iteration: with srf not
             // dividing 10, N mod S steps get one extra visit per pass
             a.q_off = pr.below(std::max<uint64_t>(G->sum.total_steps, 1));
+            a.tail_i0 = (a.units_full * 32 + a.q_off) % std::max<uint64_t>(G->sum.total_steps, 1);
             a.visits = visits.p;
             a.zhist = zhist.p;
             a.zhist_len = zhist.p ? ext.diag->zipf_draws_len : 0;

@@ -123,6 +123,13 @@ struct IterArgs {
     unsigned long long* zhist;       // [zhist_len] Zipf hops drawn
     unsigned long long* outcomes;    // [4] {uniform attempted, applied, cooling attempted, applied}
     uint32_t zhist_len;
+    // lean tile kernel (k_sgd_lean): the permutation runs over the full
+    // units only, u = (perm_a*k + perm_b) mod units_full; the partial last
+    // unit (tail_n picks, first step tail_i0) is k = units_full, the last
+    // unit of its warp, so every warp's batches stay aligned to its units
+    uint64_t units_full;
+    uint32_t tail_n;
+    uint64_t tail_i0;
 };
 
 

@@ -69,30 +69,13 @@ __device__ __forceinline__ Moments merge(const Moments& a, const Moments& b) {
 // consecutive steps -- and j uniform over the other ns - 1 steps; then up to
 // 9 coin attempts for a nonzero d_ref (metrics.cpp:116-148). Draw t of sample
 // s is the splitmix64 output at counter s*16 + t of the path's key.
-template <typename T>
-__device__ __forceinline__ bool sps_term(const DevGraph& g, const void* coords, uint64_t key, uint64_t base,
-                                         uint64_t ns, uint64_t s, uint64_t i, double& term) {
-    uint64_t j = __umul64hi(ctr_draw(key, s * 16), ns - 1);
-    j += j >= i ? 1 : 0;
-    const StepRec ri = load_step(g.step + base + i);
-    const StepRec rj = load_step(g.step + base + j);
-    for (uint64_t att = 0; att < 9; ++att) {
-        const uint64_t rr = ctr_draw(key, s * 16 + 1 + att);
-        const int ei = (rr >> 63) ? 0 : 1;
-        const int ej = ((rr >> 62) & 1) ? 0 : 1;
-        const uint64_t pi = step_pos(ri, ei), pj = step_pos(rj, ej);
-        if (pi == pj) continue;
-        const double d = abs_diff(pi, pj);
-        double vix, viy, vjx, vjy;
-        Coord<T>::get(coords, ri.node, ei, vix, viy);
-        Coord<T>::get(coords, rj.node, ej, vjx, vjy);
-        const double dx = vix - vjx, dy = viy - vjy;
-        const double err = (sqrt(dx * dx + dy * dy) - d) / d;
-        term = err * err;
-        return true;
-    }
-    return false;
-}
+#ifndef PGL_SPS_GROUP
+#define PGL_SPS_GROUP 2
+#endif
+#ifndef PGL_SPS_MINB
+#define PGL_SPS_MINB 1
+#endif
+constexpr int kGroup = PGL_SPS_GROUP;  // samples per lane in flight
 
 // One block per chunk (grid-stride): chunks are path-major -- chunk c of
 // path p covers samples [c*kChunk, min((c+1)*kChunk, spn*|p|)) of p -- so the
@@ -100,7 +83,7 @@ __device__ __forceinline__ bool sps_term(const DevGraph& g, const void* coords, 
 // once per sample. Lane l takes samples l, l+256, ...; lane moments are
 // merged by a halving tree; one Moments per chunk.
 template <typename T>
-__global__ void __launch_bounds__(kLanes) k_sps_chunks(DevGraph g, const void* __restrict__ coords, uint64_t seed,
+__global__ void __launch_bounds__(kLanes, PGL_SPS_MINB) k_sps_chunks(DevGraph g, const void* __restrict__ coords, uint64_t seed,
                                                        uint32_t spn, const uint64_t* __restrict__ chunk_cum,
                                                        uint64_t n_chunks, Moments* __restrict__ part,
                                                        unsigned long long* skipped) {
@@ -124,18 +107,67 @@ __global__ void __launch_bounds__(kLanes) k_sps_chunks(DevGraph g, const void* _
         key = splitmix_next(key);
         const uint64_t i0 = s0 % ns;
         Moments m{0.0, 0.0, 0.0};
-        for (uint64_t off = threadIdx.x; s0 + off < s_end; off += kLanes) {
-            uint64_t i = i0 + off;
-            if (ns >= kChunk) {
-                if (i >= ns) i -= ns;
-            } else {
-                i = static_cast<uint32_t>(i) % static_cast<uint32_t>(ns);
+        // kGroup samples per lane in flight: their record loads, then their
+        // coordinate loads, are issued together (memory-level parallelism);
+        // the terms are pushed in sample order, as the C restatement does
+        for (uint64_t g0 = threadIdx.x; s0 + g0 < s_end; g0 += kGroup * kLanes) {
+            StepRec ri[kGroup], rj[kGroup];
+            int ok[kGroup];
+            uint64_t pos[kGroup][2];
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) {
+                const uint64_t off = g0 + static_cast<uint64_t>(q) * kLanes;
+                ok[q] = s0 + off < s_end;
+                if (!ok[q]) continue;
+                uint64_t i = i0 + off;
+                if (ns >= kChunk) {
+                    if (i >= ns) i -= ns;
+                } else {
+                    i = static_cast<uint32_t>(i) % static_cast<uint32_t>(ns);
+                }
+                uint64_t j = __umul64hi(ctr_draw(key, (s0 + off) * 16), ns - 1);
+                j += j >= i ? 1 : 0;
+                ri[q] = load_step(g.step + base + i);
+                rj[q] = load_step(g.step + base + j);
             }
-            double t;
-            if (sps_term<T>(g, coords, key, base, ns, s0 + off, i, t))
-                push(m, t);
-            else
-                ++nsk;
+            int ends[kGroup];
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) {
+                if (!ok[q]) continue;
+                ok[q] = 0;
+                const uint64_t s = s0 + g0 + static_cast<uint64_t>(q) * kLanes;
+                for (uint64_t att = 0; att < 9; ++att) {  // metrics.cpp:116-148: up to 9 coin attempts
+                    const uint64_t rr = ctr_draw(key, s * 16 + 1 + att);
+                    const int ei = (rr >> 63) ? 0 : 1;
+                    const int ej = ((rr >> 62) & 1) ? 0 : 1;
+                    const uint64_t pi = step_pos(ri[q], ei), pj = step_pos(rj[q], ej);
+                    if (pi == pj) continue;
+                    pos[q][0] = pi;
+                    pos[q][1] = pj;
+                    ends[q] = ei | (ej << 1);
+                    ok[q] = 1;
+                    break;
+                }
+            }
+            double vix[kGroup], viy[kGroup], vjx[kGroup], vjy[kGroup];
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) {
+                if (!ok[q]) continue;
+                Coord<T>::get(coords, ri[q].node, ends[q] & 1, vix[q], viy[q]);
+                Coord<T>::get(coords, rj[q].node, ends[q] >> 1, vjx[q], vjy[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < kGroup; ++q) {
+                if (s0 + g0 + static_cast<uint64_t>(q) * kLanes >= s_end) continue;
+                if (!ok[q]) {
+                    ++nsk;
+                    continue;
+                }
+                const double d = abs_diff(pos[q][0], pos[q][1]);
+                const double dx = vix[q] - vjx[q], dy = viy[q] - vjy[q];
+                const double err = (sqrt(dx * dx + dy * dy) - d) / d;
+                push(m, err * err);
+            }
         }
         red[threadIdx.x] = m;
         __syncthreads();

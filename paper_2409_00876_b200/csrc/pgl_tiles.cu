@@ -651,6 +651,263 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
     flush_stat(stats, 7, b_second);
 }
 
+// ---- lean tile kernel (variant 7) -----------------------------------------------
+//
+// The asynchronous pipeline of k_sgd_tiles specialised to the configuration
+// every benchmark and LayoutConfig{} run uses: batch_size 32 (a unit is one
+// batch, opened by lane 0), drf 1 (no re-update combos, no warp-shuffle
+// reuse), no sampler diagnostics, S < 2^30 steps and every path shorter than
+// 2^32 nt (32-bit positions: d_ref is one 32-bit difference). Same sampler,
+// same update; what goes is the generality the default run never takes:
+//   * the permutation runs over the full units; the partial last unit is the
+//     last unit of its warp (IterArgs::units_full / tail_*), so no warp ever
+//     carries a batch across units -- no per-unit batch bookkeeping;
+//   * a group leader's shared draw (window start or Zipf hop) comes from the
+//     low 60 bits of the same generator output whose top 4 bits are its
+//     coins, instead of a second output;
+//   * the records are needed only until the partner is resolved: 2 record
+//     slots instead of 3, and the resolved update is 16 bytes (32-bit d_ref);
+//     with 64 registers and 56 KB of shared memory per 256-thread CTA, four
+//     CTAs fit an SM (variant 8) instead of three.
+struct LeanRes {
+    uint32_t ni, nj, flags, dref;
+};
+
+__host__ __device__ constexpr size_t lean_smem_bytes(bool anchored) {
+    // 2 record slots {ri, rj} + 2 endpoint slots {vi, vj, res, anchors}; a
+    // unit's selection flags wait in its res slot (free again once the unit
+    // two rounds back is applied) -- 224 bytes per lane with the anchored
+    // store's generator state, so 4 CTAs fit an SM's 228 KB
+    return static_cast<size_t>(8 * 32) * (2 * (2 * sizeof(StepRec)) +
+                                          2 * (2 * sizeof(uint4) + sizeof(LeanRes) + (anchored ? 2 * sizeof(double) : 0)));
+}
+
+// kDiag: the sampler diagnostics (pgl_layout_diag) compiled in -- the same
+// kernel for the distribution tests; the production instantiation has none.
+template <typename T, int kMinBlocks, bool kDiag>
+__global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* __restrict__ coords, DevRng rng,
+                                                               DevStats* stats, IterArgs a) {
+    const uint32_t tid = blockIdx.x * 256u + threadIdx.x;
+    const uint32_t warp = tid >> 5, lane = threadIdx.x & 31;
+    if (warp >= a.n_warps) return;
+    constexpr bool kAnch = std::is_same_v<T, AnchF32>;
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    constexpr int kW = 8;  // warps per 256-thread block
+    auto* s_ri = reinterpret_cast<StepRec(*)[kW][32]>(dyn_smem);  // [2]
+    auto* s_rj = s_ri + 2;
+    auto* s_vi = reinterpret_cast<uint4(*)[kW][32]>(s_rj + 2);    // [2]
+    auto* s_vj = s_vi + 2;
+    auto* s_res = reinterpret_cast<LeanRes(*)[kW][32]>(s_vj + 2);  // [2]
+    auto* s_ai = reinterpret_cast<double(*)[kW][32]>(s_res + 2);   // [2] (anchored)
+    auto* s_aj = s_ai + 2;
+    const int wib = static_cast<int>(threadIdx.x >> 5);
+
+    using Rng = std::conditional_t<kAnch, XoSmem, Xo>;
+    Rng r;
+    if constexpr (kAnch) {  // the register budget binds the anchored kernel
+        uint64_t* col = reinterpret_cast<uint64_t*>(dyn_smem + lean_smem_bytes(true)) + wib * 128 + lane;
+        col[0] = rng.s0[tid];
+        col[32] = rng.s1[tid];
+        col[64] = rng.s2[tid];
+        col[96] = rng.s3[tid];
+        r.s = col;
+    } else {
+        r = Xo{rng.s0[tid], rng.s1[tid], rng.s2[tid], rng.s3[tid]};
+    }
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    const uint32_t S = static_cast<uint32_t>(g.total_steps);
+    const uint32_t Uf = static_cast<uint32_t>(a.units_full);
+    const uint32_t U = Uf + (a.tail_n ? 1u : 0u);
+    const uint32_t W = a.n_warps;
+    const uint32_t N = warp < U ? (U - warp + W - 1) / W : 0;  // units k = warp + m*W < U
+    const uint32_t hl = a.hop_lanes;
+
+    uint32_t k = warp;
+    uint32_t u = k < Uf ? static_cast<uint32_t>((a.perm_a * static_cast<uint64_t>(k) + a.perm_b) % Uf) : Uf;
+    uint32_t i0 = k < Uf ? static_cast<uint32_t>((static_cast<uint64_t>(u) * 32 + a.q_off) % S)
+                         : static_cast<uint32_t>(a.tail_i0);
+    const uint32_t perm_step = static_cast<uint32_t>(a.perm_step), i0_step = static_cast<uint32_t>(a.i0_step),
+                   i0_wrap = static_cast<uint32_t>(a.i0_wrap);
+
+    uint32_t applied = 0, primary = 0, skipped = 0, b_first = 0, b_first_cool = 0, b_second = 0;
+
+    // Stage A: the unit's batch coin, i's record (coalesced), the partner.
+    auto select = [&](StepRec* dst_i, StepRec* dst_j) -> uint32_t {
+        const uint64_t out = r.next();
+        const uint32_t coins = static_cast<uint32_t>(out >> 60);
+        const bool active = u < Uf || lane < a.tail_n;
+        bool cooling;
+        if (a.force_cooling) {
+            b_second += lane == 0;
+            cooling = true;
+        } else {
+            b_first += lane == 0;
+            cooling = __shfl_sync(kFull, coins & 1u, 0);
+            b_first_cool += lane == 0 && cooling;
+        }
+        uint32_t gi = i0 + lane;
+        if (gi >= S) gi -= S;  // S >= 32 (host check)
+        if constexpr (kDiag)
+            if (a.visits != nullptr && active) atomicAdd(a.visits + gi, 1u);
+        uint32_t fl = active ? 16u : 0u;
+        fl |= cooling ? 32u : 0u;
+        // leaders: lane 0 of a uniform unit (window start), the first lane of
+        // each hop group of a cooling unit (hop, sign = its coin bit 1); the
+        // draw is the low 60 bits of the coins' output
+        const bool lead = cooling ? (lane & (hl - 1)) == 0 : lane == 0;
+        const int lsrc = cooling ? static_cast<int>(lane & ~(hl - 1)) : 0;
+        const uint64_t draw = __shfl_sync(kFull, out << 4, lsrc);
+        const uint32_t kspec = cooling ? static_cast<uint32_t>(zipf_alias(g.zalias + a.zdef_tab, a.zdef_n, draw)) : 0u;
+        uint32_t p = 0, pbase = 0, n = 0, zn = 0;
+        uint64_t zt = 0;
+        bool zdef = false;
+        if (active) p = path_of_step_fat<uint32_t>(g, a, gi, cooling, pbase, n, zn, zt, zdef);
+        // tag: bits 0-28 path, 30 draw valid, 31 hop sign
+        uint32_t tag = p;
+        if (lead && active && n >= 2) tag |= (1u << 30) | (((coins >> 1) & 1u) << 31);
+        tag = __shfl_sync(kFull, tag, lsrc);
+        const bool shared = ((tag >> 30) & 1u) && (tag & 0x1FFFFFFFu) == p;
+        cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
+        if (!active || n < 2) return fl;
+        const int32_t i = static_cast<int32_t>(gi - pbase), nn = static_cast<int32_t>(n);
+        int32_t j;
+        if (cooling) {
+            const int32_t kk = static_cast<int32_t>(shared ? (zdef ? kspec : zipf_alias(g.zalias + zt, zn, draw))
+                                                           : zipf_alias(g.zalias + zt, zn, r.next()));
+            if constexpr (kDiag)
+                if (!shared || lead) diag_zipf(a, static_cast<uint64_t>(kk));  // one count per draw
+            const int32_t sign = (shared ? (tag >> 31) : ((coins >> 1) & 1u)) ? 1 : -1;
+            j = i + sign * kk;
+            if (j < 0 || j >= nn) {
+                j = i - sign * kk;
+                if (j < 0 || j >= nn) {
+                    j = i + sign * kk;
+                    j = j < 0 ? 0 : (j > nn - 1 ? nn - 1 : j);
+                }
+            }
+            if (j == i) return fl;
+        } else {
+            if (shared) {
+                const uint32_t w0 = static_cast<uint32_t>(__umul64hi(draw, n));
+                uint32_t jj = w0 + (lane ^ static_cast<uint32_t>((draw >> 4) & 31));
+                if (jj >= n) jj = n >= 32 ? jj - n : jj % n;
+                j = static_cast<int32_t>(jj);
+            } else {
+                j = static_cast<int32_t>(r.below(n));
+            }
+            if (j == i) {
+                j = static_cast<int32_t>(r.below(n));
+                if (j == i) return fl;
+            }
+        }
+        const uint32_t gj = pbase + static_cast<uint32_t>(j);
+        fl |= 1u | ((coins & 4u) ? 0u : 2u) | ((coins & 8u) ? 0u : 4u);
+        if (gj - i0 < 32u) {  // in-tile (unsigned: gj >= i0); a wrapped unit's low part copies its own
+            fl |= 8u | ((gj - i0) << 8);
+        } else {
+            cp_async<16>(dst_j + lane, g.step + gj, pol_stream);
+        }
+        return fl;
+    };
+
+    // Round t: apply unit t-2, resolve unit t-1, select unit t. Each round
+    // commits two groups (endpoint copies of t-1, then record copies of t):
+    // apply(t-2) waits for all but the newest group, resolve(t-1) for all.
+    for (uint32_t t = 0; t < N + 2; ++t) {
+        const int cur = t & 1, prv = cur ^ 1;
+        if (t >= 2) {  // 1. apply unit t-2 (endpoint slot (t-2)&1 = cur)
+            cp_async_wait<1>();
+            const LeanRes res = s_res[cur][wib][lane];
+            const bool live = (res.flags & 1u) && res.dref != 0;
+            primary += (res.flags >> 4) & 1u;
+            skipped += ((res.flags & 16u) && !live) ? 1u : 0u;
+            if constexpr (kDiag)
+                if (res.flags & 16u) diag_outcome(a, res.flags & 32u, live);
+            if (live) {
+                const int ei = (res.flags >> 1) & 1, ej = (res.flags >> 2) & 1;
+                double vix, viy, vjx, vjy;
+                const double d = static_cast<double>(res.dref);
+                if constexpr (kAnch) {
+                    const double ai = s_ai[cur][wib][lane], aj = s_aj[cur][wib][lane];
+                    Coord<T>::decode_anchored(ei, s_vi[cur][wib][lane], ai, vix, viy);
+                    Coord<T>::decode_anchored(ej, s_vj[cur][wib][lane], aj, vjx, vjy);
+                    applied += hog_apply_io_t<T, true>(coords, res.ni, ei, res.nj, ej, d, a.eta, r, pol_keep, vix, viy,
+                                                       vjx, vjy, ai, aj);
+                } else {
+                    Coord<T>::decode(coords, res.ni, ei, s_vi[cur][wib][lane], vix, viy);
+                    Coord<T>::decode(coords, res.nj, ej, s_vj[cur][wib][lane], vjx, vjy);
+                    applied += hog_apply_io_t<T>(coords, res.ni, ei, res.nj, ej, d, a.eta, r, pol_keep, vix, viy, vjx,
+                                                 vjy);
+                }
+            }
+        }
+        if (t >= 1 && t <= N) {  // 2. resolve unit t-1 (record slot prv, endpoint slot prv)
+            cp_async_wait<0>();
+            __syncwarp();  // in-tile partners read other lanes' copies
+            const uint32_t fs = s_res[prv][wib][lane].flags;  // left there by select
+            LeanRes res{0, 0, fs & 48u, 0};
+            if (fs & 1u) {
+                const StepRec ri = s_ri[prv][wib][lane];
+                const StepRec rj = (fs & 8u) ? s_ri[prv][wib][(fs >> 8) & 31] : s_rj[prv][wib][lane];
+                const uint32_t pi = (fs & 2u) ? ri.pe_lo : ri.ps_lo, pj = (fs & 4u) ? rj.pe_lo : rj.ps_lo;
+                res = LeanRes{ri.node, rj.node, fs, pi > pj ? pi - pj : pj - pi};
+                if (res.dref) {
+                    cp_async<16>(&s_vi[prv][wib][lane], Coord<T>::copy_src(coords, ri.node, (fs >> 1) & 1), pol_keep);
+                    cp_async<16>(&s_vj[prv][wib][lane], Coord<T>::copy_src(coords, rj.node, (fs >> 2) & 1), pol_keep);
+                    if constexpr (kAnch) {
+                        cp_async<8>(&s_ai[prv][wib][lane], anch_anchor_ptr(coords, ri.node), pol_keep);
+                        cp_async<8>(&s_aj[prv][wib][lane], anch_anchor_ptr(coords, rj.node), pol_keep);
+                    }
+                }
+            }
+            s_res[prv][wib][lane] = res;
+        }
+        cp_async_commit();
+        if (t < N) {  // 3. select unit t (record slot cur)
+            if (t > 0) {
+                k += W;
+                if (k < Uf) {
+                    u += perm_step;
+                    if (u >= Uf) {
+                        u -= Uf;
+                        i0 += i0_wrap;
+                    } else {
+                        i0 += i0_step;
+                    }
+                    if (i0 >= S) i0 -= S;
+                } else {  // the partial unit: always this warp's last
+                    u = Uf;
+                    i0 = static_cast<uint32_t>(a.tail_i0);
+                }
+            }
+            s_res[cur][wib][lane].flags = select(s_ri[cur][wib], s_rj[cur][wib]);  // slot free: unit t-2 applied
+        }
+        cp_async_commit();
+        __syncwarp();
+    }
+
+    if constexpr (kAnch) {
+        rng.s0[tid] = r.s[0];
+        rng.s1[tid] = r.s[32];
+        rng.s2[tid] = r.s[64];
+        rng.s3[tid] = r.s[96];
+    } else {
+        rng.s0[tid] = r.a;
+        rng.s1[tid] = r.b;
+        rng.s2[tid] = r.c;
+        rng.s3[tid] = r.d;
+    }
+    flush_stat(stats, 0, primary);
+    flush_stat(stats, 1, primary);  // attempted = primary (drf 1)
+    flush_stat(stats, 2, applied);
+    flush_stat(stats, 3, skipped);
+    flush_stat(stats, 4, b_first);
+    flush_stat(stats, 5, b_first_cool);
+    flush_stat(stats, 6, b_second);
+    flush_stat(stats, 7, b_second);
+}
+
 // Tile-kernel variants (pgl_layout_ext.kernel_variant; 0 = auto, chosen by
 // the host):
 //   1  register pipeline, 2 CTAs/SM (no spills); auto where the concurrency
@@ -666,6 +923,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 // 64-bit index instantiation (measurements).
 template <typename T, bool k32>
 const void* tiles_fn_t(int variant) {
+    if constexpr (k32) {
+        if (variant == 7) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false>);
+        if (variant == 8) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false>);
+        if (variant == 7 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true>);
+        if (variant == 8 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true>);
+    }
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
            : variant == 6 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 1, k32>)
@@ -678,7 +941,9 @@ const void* tiles_fn(int variant, bool k32) {
 }
 
 size_t tiles_smem(int variant, int coord_kind) {
+    variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
+    if (variant == 7 || variant == 8) return lean_smem_bytes(anch) + (anch ? 256 * 4 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
     return async ? async_smem_bytes(1, anch) + (anch ? 256 * 4 * sizeof(uint64_t) : 0) : 0;
 }
@@ -697,7 +962,7 @@ LaunchShape tiles_shape(int device, int coord_kind, uint32_t max_warps, int bloc
     // 32-bit index kernel when every signed step offset i +- k stays below 2^31
     // (variant bit 4 forces the 64-bit instantiation, for measurements)
     sh.idx32 = total_steps < (1ULL << 30) && !(variant & 16);
-    variant &= 15;
+    variant &= 15 | 32;  // bit 5: the lean kernel with its diagnostics compiled in
     sh.variant = variant;
     sh.smem = tiles_smem(variant, coord_kind);
     // the async pipeline's shared-memory layout assumes 256-thread blocks

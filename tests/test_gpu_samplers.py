@@ -32,6 +32,10 @@ KERNELS = [
     pytest.param(0, 1, 1, id="tiles-v1-f64"),
     pytest.param(0, 6, 1, id="tiles-v6-f64"),
     pytest.param(0, 6, 2, id="tiles-v6-anch"),
+    pytest.param(0, 7, 1, id="tiles-v7-f64"),
+    pytest.param(0, 7, 2, id="tiles-v7-anch"),
+    pytest.param(0, 8, 1, id="tiles-v8-f64"),
+    pytest.param(0, 8, 2, id="tiles-v8-anch"),
     pytest.param(1, 0, 1, id="iid-f64"),
     pytest.param(1, 0, 2, id="iid-anch"),
 ]
@@ -64,6 +68,8 @@ def test_device_accounting_config1(pgl, gpu, samp, variant, prec):
 @pytest.mark.parametrize("samp,variant,prec", KERNELS)
 @pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (2, 3), (4, 1)])
 def test_device_accounting_reuse(pgl, gpu, samp, variant, prec, drf, srf):
+    if variant in (7, 8):
+        pytest.skip("the lean kernel covers drf 1 only (the host picks variant 6 for reuse runs)")
     g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
     st = pgl.RunStats()
     cfg = pgl.LayoutConfig(n_iters=6, drf=drf, srf=srf)
@@ -102,7 +108,7 @@ def test_device_accounting_invalid_selections(pgl, gpu):
 
 # ---- primary visits ----------------------------------------------------------------
 
-@pytest.mark.parametrize("variant", [1, 6])
+@pytest.mark.parametrize("variant", [1, 6, 8])
 @pytest.mark.parametrize("srf", [1, 3, 4, 7])
 def test_tile_visits_rotate(pgl, gpu, variant, srf):
     """The tile sampler's enumeration: in every iteration each step is the
@@ -151,6 +157,7 @@ def zipf_pmf(n, theta):
 
 
 SAMPLER_KERNELS = [pytest.param(0, 1, id="tiles-v1"), pytest.param(0, 6, id="tiles-v6"),
+                   pytest.param(0, 7, id="tiles-v7"), pytest.param(0, 8, id="tiles-v8"),
                    pytest.param(1, 0, id="iid")]
 
 
@@ -212,7 +219,7 @@ def test_zipf_draws_mixed_supports(pgl, gpu):
     walks = [[(k, 0) for k in range(30000)], [(30000 + k, 0) for k in range(10)]] + \
             [[(30010 + 10 * p + k, 0) for k in range(10)] for p in range(300)]
     g = pgl.build_graph([5] * (30010 + 3000), walks)
-    for samp, variant in [(0, 1), (0, 6), (1, 0)]:
+    for samp, variant in [(0, 1), (0, 6), (0, 8), (1, 0)]:
         d = pgl.LayoutDiag(zipf_len=1002)
         pgl.run_layout(g, pgl.LayoutConfig(n_iters=16), ext=pgl.LayoutExt(sampling=samp, kernel_variant=variant,
                                                                           diag=d))
@@ -233,13 +240,55 @@ def test_outcome_frequencies_two_step_path(pgl, gpu, samp, variant):
     """Two abutting steps of length 5: an endpoint combination collides at
     the shared position with probability 1/4; a uniform selection abandons
     1/4 of its draws (two collisions on a two-step path). So P(applied) =
-    9/16 for uniform selections and 3/4 for cooling ones, +-0.02."""
-    g = pgl.build_graph([5, 5], [[(0, 0), (1, 0)]])
+    9/16 for uniform selections and 3/4 for cooling ones, +-0.02. (The lean
+    kernels need >= 32 steps: 64 disjoint two-step paths, same frequencies.)"""
+    n_paths, n_iters = (64, 200) if variant in (7, 8) else (1, 8000)
+    g = pgl.build_graph([5] * (2 * n_paths), [[(2 * p, 0), (2 * p + 1, 0)] for p in range(n_paths)])
     d = pgl.LayoutDiag()
-    pgl.run_layout(g, pgl.LayoutConfig(n_iters=8000, global_seed=9),
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters, global_seed=9),
                    ext=pgl.LayoutExt(sampling=samp, kernel_variant=variant, diag=d))
     ua, uap, ca, cap = d.outcomes
-    assert ua + ca == 8000 * 20
+    assert ua + ca == n_iters * 20 * n_paths
     assert ua > 15000 and ca > 15000
     assert abs(uap / ua - 9 / 16) <= 0.02, uap / ua
     assert abs(cap / ca - 3 / 4) <= 0.02, cap / ca
+
+
+# ---- the lean kernel's preconditions ---------------------------------------------------
+
+def test_lean_kernel_preconditions(pgl, gpu):
+    """Variants 7/8 (k_sgd_lean) cover batch 32, drf 1, pair_window 3 and
+    32 <= S < 2^30 only; asked for anything else they refuse loudly, and the
+    auto choice never picks them there."""
+    g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
+    tiny = pgl.build_graph([4] * 6, [[(k, 0) for k in range(6)]])
+    for gg, cfg, ext in [(g, dict(batch_size=7), {}), (g, {}, dict(pair_window=2)), (tiny, {}, {}),
+                         (g, {}, dict(kernel_variant=8 | 16))]:
+        with pytest.raises(pgl.InvalidParameter):
+            pgl.run_layout(gg, pgl.LayoutConfig(n_iters=2, **cfg),
+                           ext=pgl.LayoutExt(**{"kernel_variant": 8, **ext}))
+    with pytest.raises(pgl.InvalidParameter):
+        pgl.run_layout_reuse(g, pgl.LayoutConfig(n_iters=2, drf=2, srf=2), ext=pgl.LayoutExt(kernel_variant=7))
+
+
+@pytest.mark.parametrize("variant", [7, 8])
+@pytest.mark.parametrize("prec", [0, 1, 2])
+def test_lean_kernel_batches_and_tail(pgl, gpu, variant, prec):
+    """Every unit is one batch of 32 picks opened by lane 0, the partial last
+    unit included (engine.cpp:115-124 with batch 32): the device's batch
+    counters equal ceil(N/32) per iteration, split between the halves, and
+    the first half's cooling batches are ~Bernoulli(1/2)."""
+    g = pgl.generate_synthetic_pangenome(5, 3000, 5, 0.05)
+    S = g.total_steps()
+    N = 10 * S
+    assert N % 32 != 0 or S % 32 != 0
+    st = pgl.RunStats()
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=30, global_seed=3), stats=st,
+                   ext=pgl.LayoutExt(kernel_variant=variant, coord_precision=prec))
+    units = -(-N // 32)
+    assert st.batches_first_half == 15 * units
+    assert st.batches_second_half == st.batches_second_half_cooling == 15 * units
+    frac = st.batches_first_half_cooling / st.batches_first_half
+    assert abs(frac - 0.5) < 5 / np.sqrt(st.batches_first_half), frac
+    assert st.primary_steps == st.updates_attempted == 30 * N
+    assert st.updates_applied + st.updates_skipped == st.updates_attempted
