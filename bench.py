@@ -34,7 +34,9 @@ attempted updates. (--config c1|c2|c5 select the other single-GPU configs.)
 --gpus N (torchrun): every rank lays out its own chromosome-scale graph
 (config 3's shape, generator seed 1 + rank; one chromosome per GPU, no
 collective: SURVEY.md §8e) -> weak scaling; value = all ranks' updates /
-max-over-ranks time.
+max-over-ranks time. Then (--c4 auto: when N > 1) config 4: the 24
+chromosome graphs split over the ranks by LPT, made resident, laid out back
+to back; "c4" reports the max-over-ranks makespan.
 --impl reference: times the reference CPU implementation (rank 0 only).
 """
 from __future__ import annotations
@@ -95,6 +97,8 @@ def parse():
     ap.add_argument("--coord", choices=["auto", "f32", "f64", "anch"], default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--c4", choices=["auto", "on", "off"], default="auto",
+                    help="config 4 makespan over this rank's LPT share (auto: on when N > 1)")
     return ap.parse_args()
 
 
@@ -290,6 +294,78 @@ def run_reference_arm(args, dist: Dist):
 
 # ---- our arm ----------------------------------------------------------------------
 
+# ---- config 4: 24 chromosomes over the ranks -----------------------
+
+# GRCh38 primary assembly lengths (bp), chr1..22, X, Y; config 4's backbone of
+# chromosome c is round(9.68e6 * L_c / L_chr1) (tools/c4_chromosomes.py)
+GRCH38 = [248956422, 242193529, 198295559, 190214555, 181538259, 170805979, 159345973, 145138636,
+          138394717, 133797422, 135086622, 133275309, 114364328, 107043718, 101991189, 90338345,
+          83257441, 80373285, 58617616, 64444167, 46709983, 50818468, 156040895, 57227415]
+
+
+def c4_share(n_ranks: int, rank: int):
+    """This rank's chromosomes under LPT (longest first onto the least-loaded
+    rank, ties to the lowest rank -- pgl_shard_plan's rule) by backbone size,
+    which is proportional to sum|p| and so to the updates of a layout."""
+    sizes = [int(round(9_680_000 * L / GRCH38[0])) for L in GRCH38]
+    load = [0] * n_ranks
+    mine = []
+    for c in sorted(range(len(sizes)), key=lambda k: (-sizes[k], k)):
+        r = min(range(n_ranks), key=lambda k: (load[k], k))
+        load[r] += sizes[c]
+        if r == rank:
+            mine.append(c)
+    return mine, sizes
+
+
+def run_c4(args, dist: Dist, P, ext):
+    """Config 4 on N GPUs, one rank per GPU, no collective: every rank
+    generates its LPT share of the 24 chromosome graphs and makes them resident
+    in HBM before the timed region (generation runs on the host and is not the
+    layout path), then lays them out back to back. Makespan = max over ranks of
+    the synchronised wall time of the rank's layouts (and of their summed
+    device time)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    mine, sizes = c4_share(dist.world, dist.rank)
+    t0 = time.perf_counter()
+
+    def gen(c):  # ctypes releases the GIL: graphs are generated in parallel
+        return c, P.generate_synthetic_pangenome(c + 1, sizes[c], 90, 0.05)
+
+    graphs = {}
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        for c, g in ex.map(gen, mine):
+            graphs[c] = (P.DeviceGraph(g, device=dist.local), g.total_steps())
+            del g
+    prep_s = time.perf_counter() - t0
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dev_s, upd = 0.0, 0
+    for c in mine:
+        dg, S = graphs[c]
+        cfg = P.LayoutConfig(global_seed=42 + c)
+        dg.layout(cfg, ext=ext, copy_out=False)
+        dev_s += dg.timing().device_ms / 1e3
+        upd += cfg.n_iters * 10 * S
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    for dg, _ in graphs.values():
+        dg.close()
+    makespan = dist.max(wall)
+    dev_makespan = dist.max(dev_s)
+    total_upd = dist.sum(float(upd))
+    sum_dev = dist.sum(dev_s)
+    return {"workload": "config 4: 24 synthetic chromosome graphs generate_synthetic_pangenome(c+1, "
+                        "round(9.68e6*L_c/L_chr1), 90, 0.05), LPT by backbone over the ranks, graphs resident",
+            "ranks": dist.world, "graphs_this_rank0": [f"chr{c + 1}" if c < 22 else ("chrX", "chrY")[c - 22]
+                                                        for c in mine] if dist.rank == 0 else None,
+            "updates": total_upd, "makespan_s": makespan, "device_makespan_s": dev_makespan,
+            "value": total_upd / makespan if makespan > 0 else 0.0, "unit": UNIT,
+            "lpt_ideal_s": sum_dev / dist.world, "prep_s_rank0": prep_s}
+
+
 def run_ours(args, dist: Dist):
     import paper_2409_00876_b200 as P
     import torch
@@ -379,6 +455,10 @@ def run_ours(args, dist: Dist):
     n_nodes, n_paths = g.n_nodes, g.n_paths
     del g  # the CPU sample builds the reference's own copy of the graph
 
+    c4 = None
+    if args.c4 == "on" or (args.c4 == "auto" and dist.world > 1):
+        c4 = run_c4(args, dist, P, ext)
+
     cpu = None
     if dist.rank == 0 and not args.no_cpu_baseline and args.gpus == 1:
         res = cpu_reference_sample(args, 1, args.cpu_budget_s)
@@ -422,6 +502,7 @@ def run_ours(args, dist: Dist):
                                      "model": "2 step records + 2 endpoint reads + 2 endpoint writes"},
                          "peak_source": peak_src, "ncu": ncu_cache},
             "iid_sampler": iid,
+            "c4": c4,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clk,

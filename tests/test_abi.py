@@ -177,3 +177,49 @@ d.close()
     import json
     res = json.loads(outs[0][0].strip().splitlines()[-1])
     assert res == {"value": 300.0 / 2.0, "t": 2.0, "world": 2}
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_c4_share_is_an_lpt_partition(n):
+    """bench.py's config-4 split: the ranks' shares partition the 24
+    chromosomes, follow LPT (longest first onto the least-loaded rank) and
+    stay within Graham's 4/3 bound of the ideal makespan."""
+    import bench
+    shares = [bench.c4_share(n, r)[0] for r in range(n)]
+    sizes = bench.c4_share(n, 0)[1]
+    allc = sorted(c for s in shares for c in s)
+    assert allc == list(range(24))
+    loads = [sum(sizes[c] for c in s) for s in shares]
+    assert max(loads) <= 4 / 3 * sum(sizes) / n + max(sizes)
+    # rank 0 of any split takes chr1, the largest
+    assert shares[0][0] == 0
+
+
+def test_c4_shares_two_ranks_gloo(tmp_path):
+    """The config-4 phase's plumbing over two gloo ranks: disjoint shares
+    whose union is the set, summed work and max-over-ranks makespan."""
+    script = tmp_path / "c4.py"
+    script.write_text(f"""
+import os, sys, json
+sys.path.insert(0, {ROOT!r})
+import bench
+d = bench.Dist(2)
+mine, sizes = bench.c4_share(d.world, d.rank)
+work = d.sum(float(sum(sizes[c] for c in mine)))
+ms = d.max(float(len(mine)))
+print(json.dumps({{"rank": d.rank, "mine": mine, "work": work, "max": ms}}))
+d.close()
+""")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), WORLD_SIZE="2",
+               CUDA_VISIBLE_DEVICES="")
+    procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), LOCAL_RANK=str(r)),
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
+    import json
+    res = [json.loads(o[0].strip().splitlines()[-1]) for o in outs]
+    assert sorted(res[0]["mine"] + res[1]["mine"]) == list(range(24))
+    assert not set(res[0]["mine"]) & set(res[1]["mine"])
+    import bench
+    assert res[0]["work"] == res[1]["work"] == float(sum(bench.c4_share(1, 0)[1]))
+    assert res[0]["max"] == max(len(r["mine"]) for r in res)
