@@ -138,7 +138,12 @@ typedef enum pgl_unit_order {
     PGL_ORDER_SPREAD = 1,
     /* contiguous sweep fronts: measured no faster once partners are windowed;
      * rejected (InvalidParameter) by this build, the value stays reserved */
-    PGL_ORDER_FRONTS = 2
+    PGL_ORDER_FRONTS = 2,
+    /* unit starts drawn i.i.d. uniform over the steps (with replacement), so
+     * a step's primary-visit count per iteration spreads like the
+     * reference's i.i.d. picks (Poisson-like around 10/srf) instead of being
+     * exactly N/S; lean kernel (variants 7/8) only */
+    PGL_ORDER_RANDOM = 3
 } pgl_unit_order;
 
 typedef enum pgl_coord_precision {

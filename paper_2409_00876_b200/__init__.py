@@ -52,7 +52,7 @@ MODE_HOGWILD, MODE_REPLAY = 0, 1
 COORD_F32, COORD_F64, COORD_F32_ANCHORED, COORD_AUTO = 0, 1, 2, 3
 SPS_COUNTER, SPS_STREAM = 0, 1
 SAMPLING_TILES, SAMPLING_IID = 0, 1
-ORDER_AUTO, ORDER_SPREAD, ORDER_FRONTS = 0, 1, 2
+ORDER_AUTO, ORDER_SPREAD, ORDER_FRONTS, ORDER_RANDOM = 0, 1, 2, 3
 
 _u64p = C.POINTER(C.c_uint64)
 _f64p = C.POINTER(C.c_double)

@@ -764,6 +764,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle supports fewer than 2^19 paths");
     if (ext.unit_order == PGL_ORDER_FRONTS)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the fronts order is not available in this build");
+    if (ext.unit_order > PGL_ORDER_RANDOM)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: unknown order");
     if (ext.coord_precision > PGL_COORD_AUTO)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.coord_precision: unknown coordinate store");
     if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
@@ -933,6 +935,10 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
                                   tile_variant(G->device, ext, cap, lean_ok), G->sum.total_steps);
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
+        if (ext.unit_order == PGL_ORDER_RANDOM &&
+            (ext.sampling != PGL_SAMPLING_TILES || ((shape.variant & 15) != 7 && (shape.variant & 15) != 8)))
+            raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the random order needs the lean tile kernel "
+                                             "(kernel_variant 7 or 8)");
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
     } else {
         lanes = 1;
@@ -1039,6 +1045,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             // dividing 10, N mod S steps get one extra visit per pass
             a.q_off = pr.below(std::max<uint64_t>(G->sum.total_steps, 1));
             a.tail_i0 = (a.units_full * 32 + a.q_off) % std::max<uint64_t>(G->sum.total_steps, 1);
+            a.unit_random = ext.unit_order == PGL_ORDER_RANDOM ? 1 : 0;
+            a.unit_key = pr.next();
             a.visits = visits.p;
             a.zhist = zhist.p;
             a.zhist_len = zhist.p ? ext.diag->zipf_draws_len : 0;

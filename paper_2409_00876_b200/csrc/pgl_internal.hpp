@@ -130,6 +130,10 @@ struct IterArgs {
     uint64_t units_full;
     uint32_t tail_n;
     uint64_t tail_i0;
+    // PGL_ORDER_RANDOM (lean kernel): unit k starts at step
+    // mulhi(splitmix(unit_key, k), S) instead of the permutation's
+    uint32_t unit_random;
+    uint64_t unit_key;
 };
 
 

@@ -881,6 +881,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                     i0 = static_cast<uint32_t>(a.tail_i0);
                 }
             }
+            if (a.unit_random) {  // PGL_ORDER_RANDOM: i.i.d. unit starts (counter-based, warp-uniform)
+                uint64_t z = a.unit_key + (static_cast<uint64_t>(k) + 1) * kPhi;
+                z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+                z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+                i0 = static_cast<uint32_t>(__umul64hi(z ^ (z >> 31), S));
+            }
             s_res[cur][wib][lane].flags = select(s_ri[cur][wib], s_rj[cur][wib]);  // slot free: unit t-2 applied
         }
         cp_async_commit();
