@@ -82,9 +82,9 @@ __device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const Iter
     const uint32_t p = select_path(g, x, pick);
     const uint64_t pbase = __ldg(g.cum + p);
     const int64_t n = static_cast<int64_t>(__ldg(g.cum + p + 1) - pbase);
+    if (a.visits != nullptr) atomicAdd(a.visits + pick, 1u);  // diagnostics only
     if (n < 2) return out;
     const int64_t i = static_cast<int64_t>(pick - pbase);
-    if (a.visits != nullptr) atomicAdd(a.visits + pick, 1u);  // diagnostics only
     int64_t j;
     uint64_t bits;
     if (cooling) {

@@ -441,22 +441,54 @@ def test_replay_bit_exact_nested(pgl, oracle, ref, gpu):
 
 # ---- warp-shuffle data reuse (paper §7.4) ---------------------
 
-@pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (2, 1), (4, 2)])
-def test_reuse_shuffle_accounting_and_quality(pgl, oracle, ref, gpu, drf, srf):
-    """RunStats identities of run_layout_reuse (test_engine.cpp:257-278) and
-    the acceptance #7 bar (acceptance.cpp:327-350): SPS at most 2x the drf=1
-    layout's, on config 1 (reference estimator, seed 7, spn 100)."""
-    g = pgl.generate_synthetic_pangenome(*C1)
+@pytest.fixture(scope="module")
+def c1_ref_base(pgl, ref):
+    """The reference's own drf = 1 layouts of config 1 (threads = 1, seeds
+    101-105), scored with its estimator (seed 7, spn 100): acceptance #7's base."""
     gr = ref.generate(*C1, gfa_roundtrip=True)
-    base = pgl.run_layout(g, pgl.LayoutConfig(global_seed=101))
-    st = pgl.RunStats()
-    cfg = pgl.LayoutConfig(global_seed=101, drf=drf, srf=srf)
-    out = pgl.run_layout_reuse(g, cfg, stats=st, ext=pgl.LayoutExt(reuse_shuffle=1)) if drf in (2, 4) else None
-    assert st.primary_steps == 30 * (10 * g.total_steps() // srf)
-    assert st.updates_attempted == st.primary_steps * drf
-    assert st.updates_applied + st.updates_skipped == st.updates_attempted
-    ratio = ref.sps(gr, out, 7, 100).mean / ref.sps(gr, base, 7, 100).mean
+    return gr, [ref.sps(gr, ref.run_layout(gr, make_cfg(global_seed=s))[0], 7, 100).mean for s in range(101, 106)]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (2, 1), (4, 2)])
+def test_reuse_shuffle_accounting_and_quality(pgl, oracle, ref, gpu, c1_ref_base, drf, srf):
+    """Warp-shuffle reuse (paper §7.4): RunStats identities of
+    run_layout_reuse (test_engine.cpp:257-278) and acceptance #7's bar
+    (acceptance.cpp:327-350: reuse SPS <= 2x the base layout's), with the
+    base being the REFERENCE's drf = 1 layouts -- median over seeds 101-105
+    on both sides (measured 1.02-1.19 for these settings,
+    profiles/r02_reuse_parity_c1.jsonl)."""
+    g = pgl.generate_synthetic_pangenome(*C1)
+    gr, base = c1_ref_base
+    got = []
+    for seed in range(101, 106):
+        st = pgl.RunStats()
+        cfg = pgl.LayoutConfig(global_seed=seed, drf=drf, srf=srf)
+        out = pgl.run_layout_reuse(g, cfg, stats=st, ext=pgl.LayoutExt(reuse_shuffle=1))
+        assert st.primary_steps == 30 * (10 * g.total_steps() // srf)
+        assert st.updates_attempted == st.primary_steps * drf
+        assert st.updates_applied + st.updates_skipped == st.updates_attempted
+        got.append(ref.sps(gr, out, 7, 100).mean)
+    ratio = np.median(got) / np.median(base)
     assert ratio <= 2.0, ratio
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (4, 2)])
+def test_reuse_reference_semantics_matches_reference(pgl, ref, gpu, c1_ref_base, drf, srf):
+    """The default drf > 1 semantics (re-updates of the same pair under the
+    unused endpoint combinations, engine.cpp:147-170) on the device against
+    the reference's own run_layout_reuse: median SPS over seeds 101-105
+    within 3% (measured 0.996-1.011)."""
+    g = pgl.generate_synthetic_pangenome(*C1)
+    gr, _ = c1_ref_base
+    got, want = [], []
+    for seed in range(101, 106):
+        cfg = dict(global_seed=seed, drf=drf, srf=srf)
+        got.append(ref.sps(gr, pgl.run_layout_reuse(g, pgl.LayoutConfig(**cfg)), 7, 100).mean)
+        want.append(ref.sps(gr, ref.run_layout(gr, make_cfg(**cfg), reuse=True)[0], 7, 100).mean)
+    ratio = np.median(got) / np.median(want)
+    assert 0.97 <= ratio <= 1.03, (got, want, ratio)
 
 
 def test_reuse_shuffle_rejected_outside_tiles(pgl, gpu):
