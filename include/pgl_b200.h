@@ -332,7 +332,8 @@ typedef struct pgl_timing {
                                  NonFiniteCoordinate */
     uint64_t device_threads; /* resident lanes = concurrent Hogwild workers*32 */
     uint32_t coord_kind;      /* pgl_coord_precision the layout ran with (PGL_COORD_AUTO resolved) */
-    uint32_t _pad1;
+    uint32_t kernel_variant;  /* the Hogwild kernel that ran: tile variant 1/2/5/6/7/8 (auto resolved),
+                                 0 for the i.i.d. kernel and replay */
 } pgl_timing;
 
 int pgl_graph_last_timing(const pgl_graph* g, pgl_timing* out);

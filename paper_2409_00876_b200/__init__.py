@@ -116,7 +116,7 @@ class _Timing(C.Structure):
     _fields_ = [("kernel_ms", C.c_double), ("init_ms", C.c_double), ("total_ms", C.c_double),
                 ("device_ms", C.c_double), ("launches", C.c_uint32), ("grid_blocks", C.c_uint32), ("block_threads", C.c_uint32),
                 ("nonfinite_nodes", C.c_uint32), ("device_threads", C.c_uint64),
-                ("coord_kind", C.c_uint32), ("_pad1", C.c_uint32)]
+                ("coord_kind", C.c_uint32), ("variant", C.c_uint32)]
 
 
 class _GfaInfo(C.Structure):
@@ -369,6 +369,7 @@ class Timing:
     device_threads: int
     nonfinite_nodes: int = 0
     coord_kind: int = 0
+    variant: int = 0  # tile kernel variant that ran (0: i.i.d. kernel or replay)
 
 
 # ---- graphs -----------------------------------------------------------------------
@@ -747,7 +748,7 @@ class DeviceGraph:
         t = _Timing()
         _check(_lib.pgl_graph_last_timing(self.h, C.byref(t)))
         return Timing(t.kernel_ms, t.init_ms, t.total_ms, t.device_ms, t.launches, t.grid_blocks, t.block_threads,
-                      t.device_threads, t.nonfinite_nodes, t.coord_kind)
+                      t.device_threads, t.nonfinite_nodes, t.coord_kind, t.variant)
 
     def all_finite(self, layout: Optional[np.ndarray] = None):
         """Layout::all_finite on the device: (bad node count, first bad node)

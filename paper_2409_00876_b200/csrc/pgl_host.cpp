@@ -1151,6 +1151,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     G->timing.grid_blocks = replay ? 1 : static_cast<uint32_t>(shape.blocks);
     G->timing.block_threads = replay ? 1 : static_cast<uint32_t>(shape.threads);
     G->timing.device_threads = replay ? 1 : static_cast<uint64_t>(n_warps) * 32;
+    G->timing.kernel_variant = replay || ext.sampling != PGL_SAMPLING_TILES ? 0u : static_cast<uint32_t>(shape.variant & 15);
     G->timing.total_ms = (now_s() - t_call) * 1e3;
 }
 

@@ -720,3 +720,32 @@ def test_auto_store_checks_id_locality(pgl, gpu):
         dg.layout(cfg, ext=pgl.LayoutExt(coord_precision=pgl.COORD_F32_ANCHORED), copy_out=False)
         forced = dg.stress(7, 10).mean
     assert auto <= forced
+
+
+# ---- the production kernels on a mid-size graph, against committed reference medians ----
+
+@pytest.mark.slow
+@pytest.mark.parametrize("prec", ["auto", "anch"])
+def test_production_kernel_sps_parity_mid(pgl, ref, gpu, prec):
+    """~200k nodes: the concurrency cap allows the async tile kernel, so this
+    is the kernel configs 2-5 run (the lean variant; FP64 by the auto rule,
+    and the anchored store forced). Median SPS over seeds 101-105 within 2%
+    of the reference's own layouts' median (tests/golden/mid_sps_reference.json,
+    made by tests/golden/make_mid_sps.py from oracle/_ref at 16 threads)."""
+    import json
+    with open(os.path.join(os.path.dirname(__file__), "golden", "mid_sps_reference.json")) as f:
+        gold = json.load(f)
+    args = tuple(gold["graph"]["args"])
+    g = pgl.generate_synthetic_pangenome(*args)
+    gr = ref.generate(*args)
+    assert (g.n_nodes, g.total_steps()) == (gold["graph"]["n_nodes"], gold["graph"]["total_steps"])
+    ext = pgl.LayoutExt(coord_precision=pgl.COORD_F32_ANCHORED if prec == "anch" else pgl.COORD_AUTO)
+    got = []
+    with pgl.DeviceGraph(g) as dg:
+        for seed in gold["layout"]["seeds"]:
+            lay = dg.layout(pgl.LayoutConfig(global_seed=seed), ext=ext)
+            tm = dg.timing()
+            assert tm.variant in (7, 8), tm.variant  # the production (lean async) kernel ran
+            got.append(ref.sps(gr, lay, gold["metric"]["seed"], gold["metric"]["spn"]).mean)
+    ratio = np.median(got) / gold["median_sps"]
+    assert 0.98 <= ratio <= 1.02, (got, gold["median_sps"], ratio)
