@@ -188,7 +188,13 @@ typedef struct pgl_layout_ext {
                                  under unused endpoint combinations (engine.cpp:147-170);
                                  1 = warp-level data reuse (paper §7.4): extra updates pair
                                  this lane's i with another lane's partner, from registers */
-    uint32_t _reserved[1];
+    uint32_t unit_len;        /* lean tile kernel (variants 7/8): consecutive picks per unit, a
+                                 power of two; 0 = auto (32). Below 32 needs PGL_ORDER_RANDOM:
+                                 each group of unit_len lanes takes its own i.i.d. start, and
+                                 unit_len 1 with pair_window 1 draws every primary step i.i.d.
+                                 uniform and every partner independently -- the reference's
+                                 selection distribution (weighted_step_select,
+                                 select_step_pair) on the lean pipeline */
     struct pgl_layout_diag* diag; /* sampler diagnostics (Hogwild modes), NULL = off */
 } pgl_layout_ext;
 

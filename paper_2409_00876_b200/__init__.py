@@ -73,7 +73,7 @@ class _Ext(C.Structure):
                 ("kernel_variant", C.c_uint32), ("l2_fetch_bytes", C.c_uint32),
                 ("sampling", C.c_uint32), ("unit_order", C.c_uint32), ("front_warps", C.c_uint32),
                 ("pair_window", C.c_uint32), ("record_hint", C.c_uint32), ("hop_lanes", C.c_uint32),
-                ("reuse_shuffle", C.c_uint32), ("_reserved", C.c_uint32 * 1),
+                ("reuse_shuffle", C.c_uint32), ("unit_len", C.c_uint32),
                 ("diag", C.c_void_p)]
 
 
@@ -275,6 +275,7 @@ class LayoutExt:
     record_hint: int = 0  # 0 evict_first, 1 evict_normal
     hop_lanes: int = 0  # lanes per shared Zipf hop (pair_window 3), 0 = auto
     reuse_shuffle: int = 0  # drf > 1 extras by warp-shuffle reuse (paper §7.4)
+    unit_len: int = 0  # lean kernel: picks per unit (0 = 32; below 32 needs unit_order=ORDER_RANDOM)
     # sampler diagnostics (pgl_layout_diag), counted by the Hogwild kernels
     diag: Optional["LayoutDiag"] = None
 
@@ -289,6 +290,7 @@ class LayoutExt:
         e.unit_order, e.front_warps = self.unit_order, self.front_warps
         e.pair_window, e.record_hint, e.hop_lanes = self.pair_window, self.record_hint, self.hop_lanes
         e.reuse_shuffle = self.reuse_shuffle
+        e.unit_len = self.unit_len
         if self.diag is not None:
             e.diag = C.addressof(self.diag._c())
         return e

@@ -729,7 +729,7 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
     if ((v == 7 || v == 8) && (!lean_ok || force64))
         raise(PGL_ERR_INVALID_PARAMETER,
               "pgl_layout_ext.kernel_variant 7/8 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
-              "pair_window 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
+              "pair_window 1 or 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
     return v | force64 | ((v == 7 || v == 8) && ext.diag ? 32 : 0);
 }
 
@@ -766,6 +766,10 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the fronts order is not available in this build");
     if (ext.unit_order > PGL_ORDER_RANDOM)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: unknown order");
+    if (ext.unit_len & (ext.unit_len - 1) || ext.unit_len > 32)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_len must be 0 or a power of two <= 32");
+    if (ext.unit_len && ext.unit_len < 32 && ext.unit_order != PGL_ORDER_RANDOM)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_len below 32 needs unit_order PGL_ORDER_RANDOM");
     if (ext.coord_precision > PGL_COORD_AUTO)
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.coord_precision: unknown coordinate store");
     if (ext.hop_lanes & (ext.hop_lanes - 1) || ext.hop_lanes > 32)
@@ -925,7 +929,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     uint32_t n_warps = 1;
     uint64_t lanes = 1;
     const bool lean_ok = cfg.batch_size == 32 && cfg.drf == 1 && !ext.reuse_shuffle &&
-                         (ext.pair_window == 0 || ext.pair_window == 3) && G->sum.total_steps >= 32 &&
+                         (ext.pair_window == 0 || ext.pair_window == 1 || ext.pair_window == 3) &&
+                         G->sum.total_steps >= 32 &&
                          G->sum.total_steps < (1ULL << 30) && G->sum.max_path_len < (1ULL << 32);
     if (!replay) {
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
@@ -1046,6 +1051,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             a.q_off = pr.below(std::max<uint64_t>(G->sum.total_steps, 1));
             a.tail_i0 = (a.units_full * 32 + a.q_off) % std::max<uint64_t>(G->sum.total_steps, 1);
             a.unit_random = ext.unit_order == PGL_ORDER_RANDOM ? 1 : 0;
+            a.unit_len = ext.unit_len ? ext.unit_len : 32;
             a.unit_key = pr.next();
             a.visits = visits.p;
             a.zhist = zhist.p;

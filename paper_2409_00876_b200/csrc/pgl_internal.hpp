@@ -134,6 +134,7 @@ struct IterArgs {
     // mulhi(splitmix(unit_key, k), S) instead of the permutation's
     uint32_t unit_random;
     uint64_t unit_key;
+    uint32_t unit_len;    // lean kernel: consecutive picks per unit (32; 1..16 with unit_random)
 };
 
 

@@ -722,6 +722,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
     const uint32_t W = a.n_warps;
     const uint32_t N = warp < U ? (U - warp + W - 1) / W : 0;  // units k = warp + m*W < U
     const uint32_t hl = a.hop_lanes;
+    const uint32_t ul = a.unit_len;              // lanes per unit: 32, or 1..16 with PGL_ORDER_RANDOM
+    const uint32_t gbase = lane & ~(ul - 1);     // first lane of this lane's unit
+    const bool pw_shared = a.pair_window == 3;   // shared window / Zipf hop draws (else independent partners)
 
     uint32_t k = warp;
     uint32_t u = k < Uf ? static_cast<uint32_t>((a.perm_a * static_cast<uint64_t>(k) + a.perm_b) % Uf) : Uf;
@@ -746,7 +749,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
             cooling = __shfl_sync(kFull, coins & 1u, 0);
             b_first_cool += lane == 0 && cooling;
         }
-        uint32_t gi = i0 + lane;
+        uint32_t gi = i0 + (lane - gbase);
         if (gi >= S) gi -= S;  // S >= 32 (host check)
         if constexpr (kDiag)
             if (a.visits != nullptr && active) atomicAdd(a.visits + gi, 1u);
@@ -757,17 +760,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         // draw is the low 60 bits of the coins' output
         const bool lead = cooling ? (lane & (hl - 1)) == 0 : lane == 0;
         const int lsrc = cooling ? static_cast<int>(lane & ~(hl - 1)) : 0;
-        const uint64_t draw = __shfl_sync(kFull, out << 4, lsrc);
-        const uint32_t kspec = cooling ? static_cast<uint32_t>(zipf_alias(g.zalias + a.zdef_tab, a.zdef_n, draw)) : 0u;
+        uint64_t draw = 0;
+        uint32_t kspec = 0;
+        if (pw_shared) {
+            draw = __shfl_sync(kFull, out << 4, lsrc);
+            if (cooling) kspec = static_cast<uint32_t>(zipf_alias(g.zalias + a.zdef_tab, a.zdef_n, draw));
+        }
         uint32_t p = 0, pbase = 0, n = 0, zn = 0;
         uint64_t zt = 0;
         bool zdef = false;
         if (active) p = path_of_step_fat<uint32_t>(g, a, gi, cooling, pbase, n, zn, zt, zdef);
-        // tag: bits 0-28 path, 30 draw valid, 31 hop sign
-        uint32_t tag = p;
-        if (lead && active && n >= 2) tag |= (1u << 30) | (((coins >> 1) & 1u) << 31);
-        tag = __shfl_sync(kFull, tag, lsrc);
-        const bool shared = ((tag >> 30) & 1u) && (tag & 0x1FFFFFFFu) == p;
+        bool shared = false;
+        uint32_t tag = 0;
+        if (pw_shared) {  // tag: bits 0-28 path, 30 draw valid, 31 hop sign
+            tag = p;
+            if (lead && active && n >= 2) tag |= (1u << 30) | (((coins >> 1) & 1u) << 31);
+            tag = __shfl_sync(kFull, tag, lsrc);
+            shared = ((tag >> 30) & 1u) && (tag & 0x1FFFFFFFu) == p;
+        }
         cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
         if (!active || n < 2) return fl;
         const int32_t i = static_cast<int32_t>(gi - pbase), nn = static_cast<int32_t>(n);
@@ -803,8 +813,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         }
         const uint32_t gj = pbase + static_cast<uint32_t>(j);
         fl |= 1u | ((coins & 4u) ? 0u : 2u) | ((coins & 8u) ? 0u : 4u);
-        if (gj - i0 < 32u) {  // in-tile (unsigned: gj >= i0); a wrapped unit's low part copies its own
-            fl |= 8u | ((gj - i0) << 8);
+        if (gj - i0 < ul) {  // in-unit (unsigned: gj >= i0); a wrapped unit's low part copies its own
+            fl |= 8u | ((gbase + gj - i0) << 8);
         } else {
             cp_async<16>(dst_j + lane, g.step + gj, pol_stream);
         }
@@ -881,8 +891,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                     i0 = static_cast<uint32_t>(a.tail_i0);
                 }
             }
-            if (a.unit_random) {  // PGL_ORDER_RANDOM: i.i.d. unit starts (counter-based, warp-uniform)
-                uint64_t z = a.unit_key + (static_cast<uint64_t>(k) + 1) * kPhi;
+            if (a.unit_random) {  // PGL_ORDER_RANDOM: i.i.d. unit starts (counter-based, unit-uniform)
+                uint64_t z = a.unit_key + (static_cast<uint64_t>(k) * 32 + gbase + 1) * kPhi;
                 z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
                 z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
                 i0 = static_cast<uint32_t>(__umul64hi(z ^ (z >> 31), S));
