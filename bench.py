@@ -231,6 +231,31 @@ def ncu_traffic(config: str, coord: str):
             {k: e[k] for k in keys if k in e})
 
 
+def sps_roofline(args, samples: int, kernel_ms: float, peak: float):
+    """Roofline entry of the sampled-path-stress kernel (k_sps_chunks, one
+    launch per estimate): measured DRAM bytes per sample from the committed
+    ncu --set full capture (profiles/ncu_traffic.json "<config>_<store>_sps",
+    per sample so it scales to this run's spn) x samples / the live kernel
+    time. Payload model beside it: two 16-byte step records + two endpoint
+    reads (16 B FP64, 8 B + the 8-byte block anchor anchored) per sample."""
+    payload = 32 + 2 * 16
+    out = {"kernel": "k_sps_chunks", "bound": "hbm", "unit": "GB/s", "peak": peak, "samples": samples,
+           "launch_ms": kernel_ms,
+           "payload": {"bytes_per_sample": payload,
+                       "achieved": samples * payload / (kernel_ms / 1e3) / 1e9 if kernel_ms else None}}
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            e = json.load(f)[f"{args.config}_{args.coord}_sps"]
+        bps = e["dram_bytes_per_sample"]
+        out.update({"traffic_bytes_per_sample": bps, "achieved": samples * bps / (kernel_ms / 1e3) / 1e9,
+                    "source": e.get("source")})
+        out["frac"] = out["achieved"] / peak
+    except (OSError, KeyError, ValueError, TypeError, ZeroDivisionError):
+        out.update({"achieved": None, "frac": None, "traffic_bytes_per_sample": None})
+    return out
+
+
 # ---- CPU baseline: the reference itself --------------------------------------------
 
 def cpu_reference_sample(args, n_steps_total=1, budget_s=20.0):
@@ -490,12 +515,15 @@ def run_ours(args, dist: Dist):
             "layout_wall_s": t_max / args.steps,
             "run_stats": stats,
             "sps": {"mean": sps.mean, "ci": [sps.ci_low, sps.ci_high], "n": sps.n,
-                    "method": "counter (GPU), seed 7, 100 samples/step", "kernel_ms": sps_ms},
+                    "method": "counter (GPU), seed 7, 100 samples/step", "kernel_ms": sps_ms,
+                    "roofline": sps_roofline(args, sps.n, sps_ms, peak)},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s, "api": "pgl_layout_run (C-ABI) from host PathStep arrays",
                     "bytes": "pgl_transfer_bytes deltas around the timed calls"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_sgd_tiles",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_sgd_lean" if timing.variant in (7, 8) else "k_sgd_tiles",
+                         "kernel_variant": timing.variant,
                          "model": model, "launch_ms": sgd_launch_ms, "ncu_launch_ms": ncu_ms,
                          "payload": {"bytes_per_update": payload, "achieved": payload_gbs,
                                      "frac": payload_gbs / peak,
