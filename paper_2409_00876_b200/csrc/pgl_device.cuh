@@ -291,13 +291,20 @@ __device__ __forceinline__ double abs_diff(uint64_t a, uint64_t b) {
 // stack. Reciprocal and reciprocal square root start from the MUFU 64-bit
 // approximations and are refined by Newton steps to ~1 ulp.
 
+#ifndef PGL_HOG_NR
+#define PGL_HOG_NR 2  // Newton steps after the MUFU approximation: 2 = ~1 ulp, 1 = ~2^-40 relative
+#endif
+
 __device__ __forceinline__ double rcp_nr(double b) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
     double e = fma(-b, y, 1.0);
     y = fma(y, e, y);
-    e = fma(-b, y, 1.0);
-    return fma(y, e, y);
+    if constexpr (PGL_HOG_NR >= 2) {
+        e = fma(-b, y, 1.0);
+        y = fma(y, e, y);
+    }
+    return y;
 }
 
 __device__ __forceinline__ double rsqrt_nr(double s) {
@@ -306,7 +313,8 @@ __device__ __forceinline__ double rsqrt_nr(double s) {
     const double h = 0.5 * s;
     y = y * fma(-h * y, y, 1.5);
     y = y * fma(-h * y, y, 1.5);
-    return y * fma(-h * y, y, 1.5);
+    if constexpr (PGL_HOG_NR >= 2) y = y * fma(-h * y, y, 1.5);
+    return y;
 }
 
 __device__ __forceinline__ uint64_t policy_evict_last() {

@@ -669,6 +669,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 //     slots instead of 3, and the resolved update is 16 bytes (32-bit d_ref);
 //     with 64 registers and 56 KB of shared memory per 256-thread CTA, four
 //     CTAs fit an SM (variant 8) instead of three.
+#ifndef PGL_LEAN_SMEM_RNG
+#define PGL_LEAN_SMEM_RNG 1  // anchored lean kernel: generator state in shared memory
+#endif
+
 struct LeanRes {
     uint32_t ni, nj, flags, dref;
 };
@@ -702,9 +706,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
     auto* s_aj = s_ai + 2;
     const int wib = static_cast<int>(threadIdx.x >> 5);
 
-    using Rng = std::conditional_t<kAnch, XoSmem, Xo>;
+    constexpr bool kSmemRng = kAnch && PGL_LEAN_SMEM_RNG;
+    using Rng = std::conditional_t<kSmemRng, XoSmem, Xo>;
     Rng r;
-    if constexpr (kAnch) {  // the register budget binds the anchored kernel
+    if constexpr (kSmemRng) {  // the register budget binds the anchored kernel
         uint64_t* col = reinterpret_cast<uint64_t*>(dyn_smem + lean_smem_bytes(true)) + wib * 128 + lane;
         col[0] = rng.s0[tid];
         col[32] = rng.s1[tid];
@@ -903,7 +908,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         __syncwarp();
     }
 
-    if constexpr (kAnch) {
+    if constexpr (kSmemRng) {
         rng.s0[tid] = r.s[0];
         rng.s1[tid] = r.s[32];
         rng.s2[tid] = r.s[64];
@@ -959,7 +964,8 @@ const void* tiles_fn(int variant, bool k32) {
 size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
-    if (variant == 7 || variant == 8) return lean_smem_bytes(anch) + (anch ? 256 * 4 * sizeof(uint64_t) : 0);
+    if (variant == 7 || variant == 8)
+        return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
     return async ? async_smem_bytes(1, anch) + (anch ? 256 * 4 * sizeof(uint64_t) : 0) : 0;
 }
