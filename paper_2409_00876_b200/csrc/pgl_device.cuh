@@ -187,24 +187,24 @@ __device__ __forceinline__ uint32_t select_path(const DevGraph& g, uint64_t x, u
 
 template <typename T> struct Coord;
 
-// Anchored FP32 (PGL_COORD_F32_ANCHORED): nodes in blocks of 32; a block is
-// {f64 anchor, 8 pad bytes, 32 x float4 {sx,sy,ex,ey}} = 528 bytes, x stored
-// as an f32 offset from the block's anchor (the block's first start x of the
-// initial layout). Half the bytes of FP64 per endpoint, with f32 error
-// relative to a node's displacement from its anchor, not to its absolute x
-// (which reaches 2e8 at chromosome scale, where plain f32 loses local detail).
+// Anchored FP32 (PGL_COORD_F32_ANCHORED): nodes in blocks of 32, x kept as
+// an f32 offset from the block's f64 anchor (the block's first start x,
+// re-anchored between iterations). `base` is the first node's float4
+// {sx, sy, ex, ey}; the anchors sit below it in reverse block order
+// (pgl_internal.hpp anch_bytes). Half the bytes of FP64 per endpoint, with
+// f32 error relative to a node's displacement from its anchor, not to its
+// absolute x (which reaches 2e8 at chromosome scale, where plain f32 loses
+// local detail).
 struct AnchF32 {};
 __device__ __forceinline__ const char* anch_node(const void* base, uint32_t node) {
-    return reinterpret_cast<const char*>(base) + static_cast<uint64_t>(node >> 5) * kAnchStride + 16 + (node & 31) * 16;
+    return reinterpret_cast<const char*>(base) + static_cast<uint64_t>(node) * 16;
 }
 __device__ __forceinline__ const double* anch_anchor_ptr(const void* base, uint32_t node) {
-    return reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) +
-                                           static_cast<uint64_t>(node >> 5) * kAnchStride);
+    return reinterpret_cast<const double*>(base) - 1 - (node >> 5);
 }
 __device__ __forceinline__ double anch_anchor(const void* base, uint32_t node) {
     // read-only during a layout: the L1 path is safe for the anchor word
-    return __ldg(reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) +
-                                                 static_cast<uint64_t>(node >> 5) * kAnchStride));
+    return __ldg(anch_anchor_ptr(base, node));
 }
 
 template <> struct Coord<AnchF32> {

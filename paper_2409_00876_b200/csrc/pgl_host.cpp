@@ -640,13 +640,21 @@ pgl_graph* create_graph(int device, const pgl_graph_view* v) {
     return G.release();
 }
 
+// The resident layout's store as the kernels address it (anchored: the base
+// above the block anchors, anch_base).
+const void* resident_coords(pgl_graph* G, int kind) {
+    if (kind == PGL_COORD_F64) return G->coords64.p;
+    if (kind == PGL_COORD_F32) return G->coords32.p;
+    return anch_base(G->coords32.p, G->n_nodes);
+}
+
 // The resident layout as FP64 in G->coords64 (a no-op for an FP64 layout).
 void to_f64(pgl_graph* G, int kind) {
     const uint64_t V = G->n_nodes;
     if (kind == PGL_COORD_F32)
         launch_f32_to_f64(G->coords32.p, G->coords64.p, 4 * V, G->stream);
     else if (kind == PGL_COORD_F32_ANCHORED)
-        launch_anch_to_f64(G->coords32.p, G->coords64.p, V, G->stream);
+        launch_anch_to_f64(anch_base(G->coords32.p, V), G->coords64.p, V, G->stream);
 }
 
 // pgl_graph_create_gfa: GFA -> compact steps on the host -> step records on
@@ -836,8 +844,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         coords = G->coords32.p;
     } else if (kind == PGL_COORD_F32_ANCHORED) {
         G->coords32.alloc(anch_bytes(V) / sizeof(float));
-        launch_f64_to_anch(G->coords64.p, G->coords32.p, V, G->stream);
-        coords = G->coords32.p;
+        coords = anch_base(G->coords32.p, V);
+        launch_f64_to_anch(G->coords64.p, coords, V, G->stream);
     }
 
     // per-path constants for this config (zipf_params_for, engine.cpp:36-39)
@@ -1178,7 +1186,7 @@ void graph_stress(pgl_graph* G, const double* coords, uint64_t seed, uint32_t sp
     } else {
         if (G->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
         f64 = G->layout_f64;  // pgl_coord_precision of the resident layout
-        dc = f64 == PGL_COORD_F64 ? static_cast<const void*>(G->coords64.p) : static_cast<const void*>(G->coords32.p);
+        dc = resident_coords(G, f64);
     }
     std::memset(out, 0, sizeof *out);
     if (method == PGL_SPS_COUNTER)
@@ -1568,7 +1576,7 @@ int pgl_graph_all_finite(pgl_graph* g, const double* coords, uint64_t* bad_nodes
         } else {
             if (g->layout_f64 < 0) raise(PGL_ERR_INVALID_PARAMETER, "no resident layout: run pgl_graph_layout first");
             kind = g->layout_f64;
-            dc = kind == PGL_COORD_F64 ? static_cast<const void*>(g->coords64.p) : static_cast<const void*>(g->coords32.p);
+            dc = resident_coords(g, kind);
         }
         launch_count_nonfinite(dc, kind, V, g->stats.p + 8, g->stream);
         unsigned long long r[2];

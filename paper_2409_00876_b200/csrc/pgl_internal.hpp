@@ -71,10 +71,14 @@ struct ZipfAlias {
     uint32_t alias;   // 0-based alternative column
 };
 
-// Anchored FP32 coordinate store (PGL_COORD_F32_ANCHORED): blocks of 32
-// nodes, {f64 anchor, 8 pad bytes, 32 x float4} = 528 bytes per block.
-constexpr uint64_t kAnchStride = 528;
-inline uint64_t anch_bytes(uint64_t n_nodes) { return ((n_nodes + 31) / 32) * kAnchStride; }
+// Anchored FP32 coordinate store (PGL_COORD_F32_ANCHORED): nodes in blocks
+// of 32, one f64 anchor per block. The allocation is [anchors of blocks
+// nb-1 .. 0, 8 B each, padded to 256 B][32*nb float4 {sx,sy,ex,ey}]; kernels
+// get the base = the first node: node n at base + 16 n (one IMAD.WIDE),
+// the anchor of block b at base - 8 (b + 1).
+inline uint64_t anch_anchor_bytes(uint64_t n_nodes) { return (((n_nodes + 31) / 32) * 8 + 255) & ~uint64_t{255}; }
+inline uint64_t anch_bytes(uint64_t n_nodes) { return anch_anchor_bytes(n_nodes) + ((n_nodes + 31) / 32) * 512; }
+inline void* anch_base(void* alloc, uint64_t n_nodes) { return static_cast<char*>(alloc) + anch_anchor_bytes(n_nodes); }
 
 // Everything a kernel needs to read the resident graph.
 struct DevGraph {

@@ -256,28 +256,28 @@ void launch_sgd_hogwild(const DevGraph& g, void* coords, int coord_kind, DevRng 
     PGL_CUDA(cudaGetLastError());
 }
 
-// FP64 layout <-> anchored FP32 store (one thread per node)
+// FP64 layout <-> anchored FP32 store (one thread per node); `dst`/`src`
+// is the store's base (anch_base): node n at base + 16 n, block b's anchor
+// at base - 8 (b + 1)
 __global__ void k_f64_to_anch(const double* __restrict__ src, char* __restrict__ dst, uint64_t V) {
     for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < V;
          n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        char* blk = dst + (n >> 5) * kAnchStride;
         const double anchor = src[4 * (n & ~static_cast<uint64_t>(31))];  // the block's first start x
-        if ((n & 31) == 0) *reinterpret_cast<double*>(blk) = anchor;
+        if ((n & 31) == 0) *(reinterpret_cast<double*>(dst) - 1 - (n >> 5)) = anchor;
         float4 f;
         f.x = static_cast<float>(src[4 * n] - anchor);
         f.y = static_cast<float>(src[4 * n + 1]);
         f.z = static_cast<float>(src[4 * n + 2] - anchor);
         f.w = static_cast<float>(src[4 * n + 3]);
-        *reinterpret_cast<float4*>(blk + 16 + (n & 31) * 16) = f;
+        *reinterpret_cast<float4*>(dst + 16 * n) = f;
     }
 }
 
 __global__ void k_anch_to_f64(const char* __restrict__ src, double* __restrict__ dst, uint64_t V) {
     for (uint64_t n = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; n < V;
          n += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const char* blk = src + (n >> 5) * kAnchStride;
-        const double anchor = *reinterpret_cast<const double*>(blk);
-        const float4 f = *reinterpret_cast<const float4*>(blk + 16 + (n & 31) * 16);
+        const double anchor = *(reinterpret_cast<const double*>(src) - 1 - (n >> 5));
+        const float4 f = *reinterpret_cast<const float4*>(src + 16 * n);
         dst[4 * n] = anchor + static_cast<double>(f.x);
         dst[4 * n + 1] = f.y;
         dst[4 * n + 2] = anchor + static_cast<double>(f.z);
@@ -294,19 +294,20 @@ __global__ void k_reanchor(char* __restrict__ store, uint64_t V) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nblocks = (V + 31) / 32;
     for (uint64_t b = warp; b < nblocks; b += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
-        char* blk = store + b * kAnchStride;
-        const double a_old = *reinterpret_cast<const double*>(blk);
-        const float dx0 = *reinterpret_cast<const float*>(blk + 16);  // node 0's start x offset
+        double* anc = reinterpret_cast<double*>(store) - 1 - b;
+        char* blk = store + b * 512;
+        const double a_old = *anc;
+        const float dx0 = *reinterpret_cast<const float*>(blk);  // node 0's start x offset
         const double a_new = a_old + static_cast<double>(dx0);
         if (b * 32 + lane < V) {
-            float4* f = reinterpret_cast<float4*>(blk + 16 + lane * 16);
+            float4* f = reinterpret_cast<float4*>(blk + lane * 16);
             float4 v = *f;
             v.x = static_cast<float>(a_old + static_cast<double>(v.x) - a_new);
             v.z = static_cast<float>(a_old + static_cast<double>(v.z) - a_new);
             *f = v;
         }
         __syncwarp();
-        if (lane == 0) *reinterpret_cast<double*>(blk) = a_new;
+        if (lane == 0) *anc = a_new;
     }
 }
 

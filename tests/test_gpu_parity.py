@@ -10,6 +10,8 @@ Bars:
   * Hogwild layouts: RunStats identities exact (test_engine.cpp:257-312),
     median SPS over seeds 101..105 within 2% of the reference (north star)
 """
+import os
+
 import numpy as np
 import pytest
 
