@@ -682,8 +682,11 @@ __host__ __device__ constexpr size_t lean_smem_bytes(bool anchored) {
     // unit's selection flags wait in its res slot (free again once the unit
     // two rounds back is applied) -- 224 bytes per lane with the anchored
     // store's generator state, so 4 CTAs fit an SM's 228 KB
-    return static_cast<size_t>(8 * 32) * (2 * (2 * sizeof(StepRec)) +
-                                          2 * (2 * sizeof(uint4) + sizeof(LeanRes) + (anchored ? 2 * sizeof(double) : 0)));
+    // (anchored: an endpoint is the 8-byte float2 half of its node's record
+    // plus the 8-byte block anchor)
+    return static_cast<size_t>(8 * 32) *
+           (2 * (2 * sizeof(StepRec)) +
+            2 * (sizeof(LeanRes) + (anchored ? 2 * (sizeof(float2) + sizeof(double)) : 2 * sizeof(uint4))));
 }
 
 // kDiag: the sampler diagnostics (pgl_layout_diag) compiled in -- the same
@@ -699,11 +702,15 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
     constexpr int kW = 8;  // warps per 256-thread block
     auto* s_ri = reinterpret_cast<StepRec(*)[kW][32]>(dyn_smem);  // [2]
     auto* s_rj = s_ri + 2;
-    auto* s_vi = reinterpret_cast<uint4(*)[kW][32]>(s_rj + 2);    // [2]
+    auto* s_res = reinterpret_cast<LeanRes(*)[kW][32]>(s_rj + 2);  // [2]
+    // endpoints [2]: FP64 / f32 the copied 16-byte record; anchored the
+    // float2 half (start or end) of the node's record and its block anchor
+    auto* s_vi = reinterpret_cast<uint4(*)[kW][32]>(s_res + 2);
     auto* s_vj = s_vi + 2;
-    auto* s_res = reinterpret_cast<LeanRes(*)[kW][32]>(s_vj + 2);  // [2]
-    auto* s_ai = reinterpret_cast<double(*)[kW][32]>(s_res + 2);   // [2] (anchored)
+    auto* s_ai = reinterpret_cast<double(*)[kW][32]>(s_res + 2);
     auto* s_aj = s_ai + 2;
+    auto* s_hi = reinterpret_cast<float2(*)[kW][32]>(s_aj + 2);
+    auto* s_hj = s_hi + 2;
     const int wib = static_cast<int>(threadIdx.x >> 5);
 
     constexpr bool kSmemRng = kAnch && PGL_LEAN_SMEM_RNG;
@@ -845,8 +852,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const double d = static_cast<double>(res.dref);
                 if constexpr (kAnch) {
                     const double ai = s_ai[cur][wib][lane], aj = s_aj[cur][wib][lane];
-                    Coord<T>::decode_anchored(ei, s_vi[cur][wib][lane], ai, vix, viy);
-                    Coord<T>::decode_anchored(ej, s_vj[cur][wib][lane], aj, vjx, vjy);
+                    const float2 hi = s_hi[cur][wib][lane], hj = s_hj[cur][wib][lane];
+                    vix = ai + static_cast<double>(hi.x);
+                    viy = static_cast<double>(hi.y);
+                    vjx = aj + static_cast<double>(hj.x);
+                    vjy = static_cast<double>(hj.y);
                     applied += hog_apply_io_t<T, true>(coords, res.ni, ei, res.nj, ej, d, a.eta, r, pol_keep, vix, viy,
                                                        vjx, vjy, ai, aj);
                 } else {
@@ -868,11 +878,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const uint32_t pi = (fs & 2u) ? ri.pe_lo : ri.ps_lo, pj = (fs & 4u) ? rj.pe_lo : rj.ps_lo;
                 res = LeanRes{ri.node, rj.node, fs, pi > pj ? pi - pj : pj - pi};
                 if (res.dref) {
-                    cp_async<16>(&s_vi[prv][wib][lane], Coord<T>::copy_src(coords, ri.node, (fs >> 1) & 1), pol_keep);
-                    cp_async<16>(&s_vj[prv][wib][lane], Coord<T>::copy_src(coords, rj.node, (fs >> 2) & 1), pol_keep);
                     if constexpr (kAnch) {
+                        cp_async<8>(&s_hi[prv][wib][lane], anch_node(coords, ri.node) + 8 * ((fs >> 1) & 1), pol_keep);
+                        cp_async<8>(&s_hj[prv][wib][lane], anch_node(coords, rj.node) + 8 * ((fs >> 2) & 1), pol_keep);
                         cp_async<8>(&s_ai[prv][wib][lane], anch_anchor_ptr(coords, ri.node), pol_keep);
                         cp_async<8>(&s_aj[prv][wib][lane], anch_anchor_ptr(coords, rj.node), pol_keep);
+                    } else {
+                        cp_async<16>(&s_vi[prv][wib][lane], Coord<T>::copy_src(coords, ri.node, (fs >> 1) & 1),
+                                     pol_keep);
+                        cp_async<16>(&s_vj[prv][wib][lane], Coord<T>::copy_src(coords, rj.node, (fs >> 2) & 1),
+                                     pol_keep);
                     }
                 }
             }
