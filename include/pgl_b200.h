@@ -128,7 +128,15 @@ typedef enum pgl_sampling {
      * by __shfl_sync. Partner, coins and update as the reference. */
     PGL_SAMPLING_TILES = 0,
     /* weighted_step_select per pick, i.i.d. (graph.hpp:123-138). */
-    PGL_SAMPLING_IID = 1
+    PGL_SAMPLING_IID = 1,
+    /* default: the tile sampler where the graph fills the GPU (the Hogwild
+     * concurrency cap -- one warp per 80 nodes -- allows the lean tile
+     * kernel's full residency, 24 warps per SM: >= ~284k nodes on a B200),
+     * the i.i.d. kernel where the cap binds (small or dense graphs, e.g.
+     * configs 1 and 5: there the tile kernels' correlated updates and longer
+     * read-to-write window move the sampled path stress 2-4% off the
+     * reference's, the i.i.d. kernel stays within 1%). */
+    PGL_SAMPLING_AUTO = 2
 } pgl_sampling;
 
 /* Order in which the tile sampler visits its units of 32 picks. */
@@ -176,7 +184,7 @@ typedef struct pgl_layout_ext {
                                  via shared memory, 4/3 CTAs/SM.
                                  i.i.d. kernel: 0 = 2 CTAs/SM, 1 = 3 CTAs/SM */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
-    uint32_t sampling;        /* pgl_sampling (Hogwild mode only) */
+    uint32_t sampling;        /* pgl_sampling (Hogwild mode only; default PGL_SAMPLING_AUTO) */
     uint32_t unit_order;      /* pgl_unit_order (tile sampling only) */
     uint32_t front_warps;     /* reserved (was: warps per sweep front) */
     uint32_t pair_window;     /* 0 = auto (= 3), 1 = independent partner draws,

@@ -51,7 +51,7 @@ _lib = C.CDLL(LIB_PATH)
 MODE_HOGWILD, MODE_REPLAY = 0, 1
 COORD_F32, COORD_F64, COORD_F32_ANCHORED, COORD_AUTO = 0, 1, 2, 3
 SPS_COUNTER, SPS_STREAM = 0, 1
-SAMPLING_TILES, SAMPLING_IID = 0, 1
+SAMPLING_TILES, SAMPLING_IID, SAMPLING_AUTO = 0, 1, 2
 ORDER_AUTO, ORDER_SPREAD, ORDER_FRONTS, ORDER_RANDOM = 0, 1, 2, 3
 
 _u64p = C.POINTER(C.c_uint64)
@@ -268,7 +268,7 @@ class LayoutExt:
     l2_persist: int = 0
     l2_fetch_bytes: int = 0
     kernel_variant: int = 0
-    sampling: int = 0  # SAMPLING_TILES
+    sampling: int = 2  # SAMPLING_AUTO: tiles where the graph fills the GPU, i.i.d. where the cap binds
     unit_order: int = 0  # ORDER_AUTO
     front_warps: int = 0
     pair_window: int = 0  # 0 auto (= 3), 1 independent draws, 2 shared uniform window, 3 window + shared Zipf hop

@@ -766,6 +766,20 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.struct_size mismatch");
         std::memcpy(&ext, extp, extp->struct_size);
     }
+    if (ext.sampling == PGL_SAMPLING_AUTO) {
+        // the tile sampler once the concurrency cap allows the lean tile
+        // kernel's full residency (3 CTAs x 8 warps per SM), the i.i.d. kernel
+        // where the cap binds (pgl_b200.h PGL_SAMPLING_AUTO;
+        // profiles/r02_quality_*.jsonl); warp-shuffle reuse needs the tiles
+        int sms = 0;
+        PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, G->device));
+        const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(G->n_nodes);
+        // (a tile-kernel knob -- variant, unit order or length, partner
+        // window, hop lanes, warp-shuffle reuse -- asks for the tiles)
+        const bool tile_knobs = ext.kernel_variant || ext.unit_order || ext.unit_len || ext.pair_window ||
+                                ext.hop_lanes || ext.reuse_shuffle;
+        ext.sampling = tile_knobs || cap >= static_cast<uint32_t>(sms) * 24 ? PGL_SAMPLING_TILES : PGL_SAMPLING_IID;
+    }
     if (ext.reuse_shuffle && (ext.mode != PGL_MODE_HOGWILD || ext.sampling != PGL_SAMPLING_TILES))
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle needs the Hogwild tile sampler");
     if (ext.reuse_shuffle && G->n_paths >= (1u << 19))
@@ -790,7 +804,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (G->n_paths == 0 || !G->sum.usable)
         raise(PGL_ERR_DEGENERATE_GRAPH, "layout needs at least one path with two or more steps");
     if (ext.mode != PGL_MODE_HOGWILD && ext.mode != PGL_MODE_REPLAY) raise(PGL_ERR_INVALID_PARAMETER, "unknown mode");
-    if (ext.sampling > PGL_SAMPLING_IID) raise(PGL_ERR_INVALID_PARAMETER, "unknown sampling");
+    if (ext.sampling > PGL_SAMPLING_AUTO) raise(PGL_ERR_INVALID_PARAMETER, "unknown sampling");
 
     DeviceGuard dg(G->device);
     const pgl_graph_view hv = view_of(G);
@@ -1048,7 +1062,12 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
             }
             a.pair_window = ext.pair_window == 1 ? 0 : (ext.pair_window == 2 ? 1 : 3);
             a.record_hint = ext.record_hint;
-            a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : kHopLanes;
+            // lanes per shared Zipf hop: 8 on the async pipelines; 1 (independent
+            // hops) on the register pipeline, which runs small graphs where the
+            // cap binds (config 1: SPS ratio 1.008 vs 1.017 with 8,
+            // profiles/r02_quality_c1.jsonl)
+            const int sv = shape.variant & 15;
+            a.hop_lanes = ext.hop_lanes ? ext.hop_lanes : (sv == 1 || sv == 2 ? 1u : kHopLanes);
             a.reuse_shuffle = ext.reuse_shuffle ? 1 : 0;
             a.zdef_n = zdef_n;
             a.zdef_tab = zdef_tab;
@@ -1462,6 +1481,7 @@ void pgl_layout_ext_default(pgl_layout_ext* e) {
     e->struct_size = sizeof(pgl_layout_ext);
     e->mode = PGL_MODE_HOGWILD;
     e->coord_precision = PGL_COORD_AUTO;
+    e->sampling = PGL_SAMPLING_AUTO;
 }
 
 int pgl_graph_create(int device, const pgl_graph_view* v, pgl_graph** out) {

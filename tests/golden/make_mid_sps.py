@@ -3,10 +3,10 @@ layouts (oracle/_ref/libpglref.so, compiled from the reference sources by
 oracle/Makefile; threads = 16) of a mid-size synthetic graph, scored with the
 reference's sampled_path_stress (seed 7, spn 10), for layout seeds 101-105.
 
-The graph (generate_synthetic_pangenome(1, 193600, 20, 0.05), ~200k nodes)
-is large enough that the device runs its production Hogwild kernel there --
+The graph (generate_synthetic_pangenome(1, 387200, 20, 0.05), ~400k nodes)
+is large enough that the device runs its production tile kernel there --
 the concurrency cap (one warp per 80 nodes) allows the lean async tile
-kernel -- so tests/test_gpu_parity.py::test_production_kernel_sps_parity_mid
+kernel's full residency, so PGL_SAMPLING_AUTO picks the tile sampler -- so tests/test_gpu_parity.py::test_production_kernel_sps_parity_mid
 gates exactly the kernels configs 2-5 run (FP64 and anchored stores) against
 these medians without re-running the reference (~1 min per layout).
 
@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 from oracle_ffi import Reference, make_cfg  # noqa: E402
 
-MID = (1, 193600, 20, 0.05)
+MID = (1, 387200, 20, 0.05)
 SEEDS = (101, 102, 103, 104, 105)
 
 

@@ -406,28 +406,33 @@ def test_nested_graph_index_matches_reference(pgl, ref, gpu):
 
 @pytest.mark.slow
 def test_hogwild_sps_parity_config5(pgl, ref, gpu):
-    """Quality gate on the high-complexity shape (inversions, duplications,
-    long Zipf jumps: zipf_space_max 1e5), median SPS over seeds 101..105 vs
-    the reference's threads=1 layouts, same estimator and metric seed.
-    * the i.i.d. sampler (the reference's selection distribution) lands within
-      2% of the reference (measured 0.99);
-    * the default tile sampler is never worse than the reference by more than
-      2%; on this shape its layouts come out ~3% LOWER in stress (measured
-      0.97: shared Zipf hops move blocks of a path coherently, which helps
-      around inversions and duplications; profiles/r01_c5_quality_small.jsonl)."""
+    """Quality gate on the high-complexity shape (nested bubbles, inversions,
+    duplications, long Zipf jumps: zipf_space_max 1e5), median SPS over
+    seeds 101..105 vs the reference's threads=1 layouts, same estimator and
+    metric seed, two-sided +-2%:
+    * the default (PGL_SAMPLING_AUTO) resolves to the i.i.d. kernel here --
+      the concurrency cap binds on this graph -- and lands within 1% (0.991
+      over 10 seeds, 0.9925 at full size vs 16-thread reference layouts,
+      profiles/r02_quality_c5small.jsonl, r02_quality_c5full.jsonl);
+    * the explicit i.i.d. sampler likewise.
+    (The tile sampler, which the default does not pick here, measures
+    0.96-0.98 on this shape: its correlated updates and the async pipeline's
+    read-to-write window move this dense graph's layout off the reference's.)"""
     g, gr = nested_pair(pgl, ref, C5_SMALL)
-    tiles, iid, cpu = [], [], []
-    for seed in range(101, 106):
-        cfg = dict(global_seed=seed, zipf_space_max=100000)
-        tiles.append(ref.sps(gr, pgl.run_layout(g, pgl.LayoutConfig(**cfg)), 7, 20).mean)
-        out = pgl.run_layout(g, pgl.LayoutConfig(**cfg), ext=pgl.LayoutExt(sampling=pgl.SAMPLING_IID))
-        iid.append(ref.sps(gr, out, 7, 20).mean)
-        lay, _ = ref.run_layout(gr, make_cfg(**cfg))
-        cpu.append(ref.sps(gr, lay, 7, 20).mean)
+    auto, iid, cpu = [], [], []
+    with pgl.DeviceGraph(g) as dg:
+        for seed in range(101, 106):
+            cfg = dict(global_seed=seed, zipf_space_max=100000)
+            auto.append(ref.sps(gr, dg.layout(pgl.LayoutConfig(**cfg)), 7, 20).mean)
+            assert dg.timing().variant == 0  # auto -> the i.i.d. kernel
+            out = dg.layout(pgl.LayoutConfig(**cfg), ext=pgl.LayoutExt(sampling=pgl.SAMPLING_IID))
+            iid.append(ref.sps(gr, out, 7, 20).mean)
+            lay, _ = ref.run_layout(gr, make_cfg(**cfg))
+            cpu.append(ref.sps(gr, lay, 7, 20).mean)
     r_iid = np.median(iid) / np.median(cpu)
-    r_tiles = np.median(tiles) / np.median(cpu)
+    r_auto = np.median(auto) / np.median(cpu)
     assert 0.98 <= r_iid <= 1.02, (iid, cpu, r_iid)
-    assert r_tiles <= 1.02, (tiles, cpu, r_tiles)
+    assert 0.98 <= r_auto <= 1.02, (auto, cpu, r_auto)
 
 
 def test_replay_bit_exact_nested(pgl, oracle, ref, gpu):
@@ -729,9 +734,10 @@ def test_auto_store_checks_id_locality(pgl, gpu):
 @pytest.mark.slow
 @pytest.mark.parametrize("prec", ["auto", "anch"])
 def test_production_kernel_sps_parity_mid(pgl, ref, gpu, prec):
-    """~200k nodes: the concurrency cap allows the async tile kernel, so this
-    is the kernel configs 2-5 run (the lean variant; FP64 by the auto rule,
-    and the anchored store forced). Median SPS over seeds 101-105 within 2%
+    """~400k nodes: the concurrency cap allows the lean tile kernel's full
+    residency, so the default picks the tile sampler -- this is the kernel
+    configs 2-4 run (the lean variant; FP64 by the auto rule, and the
+    anchored store forced). Median SPS over seeds 101-105 within 2%
     of the reference's own layouts' median (tests/golden/mid_sps_reference.json,
     made by tests/golden/make_mid_sps.py from oracle/_ref at 16 threads)."""
     import json
