@@ -669,6 +669,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 //     slots instead of 3, and the resolved update is 16 bytes (32-bit d_ref);
 //     with 64 registers and 56 KB of shared memory per 256-thread CTA, four
 //     CTAs fit an SM (variant 8) instead of three.
+#ifndef PGL_LEAN_BULK
+#define PGL_LEAN_BULK 1  // unit records staged by one cp.async.bulk (TMA) per warp round
+#endif
 #ifndef PGL_LEAN_SMEM_RNG
 #define PGL_LEAN_SMEM_RNG 0  // 1: anchored lean kernel keeps its generator state in shared memory (C3: 51.6 vs 53.6 G upd/s in registers)
 #endif
@@ -730,6 +733,19 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
     const uint64_t pol_stream = policy_evict_first();
     const uint32_t S = static_cast<uint32_t>(g.total_steps);
     const uint32_t Uf = static_cast<uint32_t>(a.units_full);
+    // one mbarrier per record slot of this warp: a full unit's 32 records
+    // (512 contiguous bytes) arrive by one bulk copy through the TMA engine
+    // instead of 32 lane copies through the LSU pipe (PGL_LEAN_BULK)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dyn_smem + lean_smem_bytes(kAnch) +
+                                                 (kSmemRng ? kW * 32 * 4 * sizeof(uint64_t) : 0)) + wib * 2;
+    if constexpr (PGL_LEAN_BULK) {
+        if (lane == 0) {
+            mbar_init(bars, 1);
+            mbar_init(bars + 1, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     const uint32_t U = Uf + (a.tail_n ? 1u : 0u);
     const uint32_t W = a.n_warps;
     const uint32_t N = warp < U ? (U - warp + W - 1) / W : 0;  // units k = warp + m*W < U
@@ -790,7 +806,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
             tag = __shfl_sync(kFull, tag, lsrc);
             shared = ((tag >> 30) & 1u) && (tag & 0x1FFFFFFFu) == p;
         }
-        cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
+        if constexpr (PGL_LEAN_BULK) {
+            // a full unit that does not wrap past S and starts the warp's
+            // lanes together: one 512-byte bulk copy; otherwise lane copies
+            // and a plain arrival so the slot's phase completes either way
+            uint64_t* bar = bars + (dst_i == s_ri[0][wib] ? 0 : 1);
+            if (ul == 32 && u < Uf && i0 <= S - 32) {
+                if (lane == 0) {
+                    fence_proxy_async_smem();  // the slot's previous reads (generic proxy) come first
+                    mbar_arrive_tx(bar, 32 * sizeof(StepRec));
+                    tma_load_hint(dst_i, g.step + i0, 32 * sizeof(StepRec), bar, pol_stream);
+                }
+            } else {
+                cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
+                if (lane == 0) mbar_arrive(bar);
+            }
+        } else {
+            cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
+        }
         if (!active || n < 2) return fl;
         const int32_t i = static_cast<int32_t>(gi - pbase), nn = static_cast<int32_t>(n);
         int32_t j;
@@ -869,6 +902,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         }
         if (t >= 1 && t <= N) {  // 2. resolve unit t-1 (record slot prv, endpoint slot prv)
             cp_async_wait<0>();
+            if constexpr (PGL_LEAN_BULK) mbar_wait(bars + prv, ((t - 1) >> 1) & 1u);  // unit t-1's records
             __syncwarp();  // in-tile partners read other lanes' copies
             const uint32_t fs = s_res[prv][wib][lane].flags;  // left there by select
             LeanRes res{0, 0, fs & 48u, 0};
@@ -980,7 +1014,8 @@ size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
     if (variant == 7 || variant == 8)
-        return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0);
+        return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0) +
+               (PGL_LEAN_BULK ? 8 * 2 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
     return async ? async_smem_bytes(1, anch) + (anch ? 256 * 4 * sizeof(uint64_t) : 0) : 0;
 }
