@@ -907,21 +907,22 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
             const uint32_t fs = s_res[prv][wib][lane].flags;  // left there by select
             LeanRes res{0, 0, fs & 48u, 0};
             if (fs & 1u) {
-                const StepRec ri = s_ri[prv][wib][lane];
-                const StepRec rj = (fs & 8u) ? s_ri[prv][wib][(fs >> 8) & 31] : s_rj[prv][wib][lane];
-                const uint32_t pi = (fs & 2u) ? ri.pe_lo : ri.ps_lo, pj = (fs & 4u) ? rj.pe_lo : rj.ps_lo;
-                res = LeanRes{ri.node, rj.node, fs, pi > pj ? pi - pj : pj - pi};
+                // two 32-bit words of each record (node, the coin's position):
+                // 1 shared-memory wavefront each instead of 4 for the record
+                const uint32_t* wi = &s_ri[prv][wib][lane].node;
+                const uint32_t* wj = (fs & 8u) ? &s_ri[prv][wib][(fs >> 8) & 31].node : &s_rj[prv][wib][lane].node;
+                const uint32_t ni = wi[0], nj = wj[0];
+                const uint32_t pi = wi[(fs & 2u) ? 2 : 1], pj = wj[(fs & 4u) ? 2 : 1];  // pe_lo : ps_lo
+                res = LeanRes{ni, nj, fs, pi > pj ? pi - pj : pj - pi};
                 if (res.dref) {
                     if constexpr (kAnch) {
-                        cp_async<8>(&s_hi[prv][wib][lane], anch_node(coords, ri.node) + 8 * ((fs >> 1) & 1), pol_keep);
-                        cp_async<8>(&s_hj[prv][wib][lane], anch_node(coords, rj.node) + 8 * ((fs >> 2) & 1), pol_keep);
-                        cp_async<8>(&s_ai[prv][wib][lane], anch_anchor_ptr(coords, ri.node), pol_keep);
-                        cp_async<8>(&s_aj[prv][wib][lane], anch_anchor_ptr(coords, rj.node), pol_keep);
+                        cp_async<8>(&s_hi[prv][wib][lane], anch_node(coords, ni) + 8 * ((fs >> 1) & 1), pol_keep);
+                        cp_async<8>(&s_hj[prv][wib][lane], anch_node(coords, nj) + 8 * ((fs >> 2) & 1), pol_keep);
+                        cp_async<8>(&s_ai[prv][wib][lane], anch_anchor_ptr(coords, ni), pol_keep);
+                        cp_async<8>(&s_aj[prv][wib][lane], anch_anchor_ptr(coords, nj), pol_keep);
                     } else {
-                        cp_async<16>(&s_vi[prv][wib][lane], Coord<T>::copy_src(coords, ri.node, (fs >> 1) & 1),
-                                     pol_keep);
-                        cp_async<16>(&s_vj[prv][wib][lane], Coord<T>::copy_src(coords, rj.node, (fs >> 2) & 1),
-                                     pol_keep);
+                        cp_async<16>(&s_vi[prv][wib][lane], Coord<T>::copy_src(coords, ni, (fs >> 1) & 1), pol_keep);
+                        cp_async<16>(&s_vj[prv][wib][lane], Coord<T>::copy_src(coords, nj, (fs >> 2) & 1), pol_keep);
                     }
                 }
             }
