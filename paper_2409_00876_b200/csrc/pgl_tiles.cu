@@ -694,7 +694,10 @@ __host__ __device__ constexpr size_t lean_smem_bytes(bool anchored) {
 
 // kDiag: the sampler diagnostics (pgl_layout_diag) compiled in -- the same
 // kernel for the distribution tests; the production instantiation has none.
-template <typename T, int kMinBlocks, bool kDiag>
+// kSync (variant 9): the endpoints are not staged a round ahead; apply reads
+// them from L2 and writes them back at once -- a read-to-write window of one
+// L2 round trip, as the i.i.d. kernel has (the staged window is a full round).
+template <typename T, int kMinBlocks, bool kDiag, bool kSync = false>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                DevStats* stats, IterArgs a) {
     const uint32_t tid = blockIdx.x * 256u + threadIdx.x;
@@ -883,7 +886,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const int ei = (res.flags >> 1) & 1, ej = (res.flags >> 2) & 1;
                 double vix, viy, vjx, vjy;
                 const double d = static_cast<double>(res.dref);
-                if constexpr (kAnch) {
+                if constexpr (kSync) {
+                    CoordHint<T>::get(coords, res.ni, ei, pol_keep, vix, viy);
+                    CoordHint<T>::get(coords, res.nj, ej, pol_keep, vjx, vjy);
+                    applied += hog_apply_io_t<T>(coords, res.ni, ei, res.nj, ej, d, a.eta, r, pol_keep, vix, viy, vjx,
+                                                 vjy);
+                } else if constexpr (kAnch) {
                     const double ai = s_ai[cur][wib][lane], aj = s_aj[cur][wib][lane];
                     const float2 hi = s_hi[cur][wib][lane], hj = s_hj[cur][wib][lane];
                     vix = ai + static_cast<double>(hi.x);
@@ -914,7 +922,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const uint32_t ni = wi[0], nj = wj[0];
                 const uint32_t pi = wi[(fs & 2u) ? 2 : 1], pj = wj[(fs & 4u) ? 2 : 1];  // pe_lo : ps_lo
                 res = LeanRes{ni, nj, fs, pi > pj ? pi - pj : pj - pi};
-                if (res.dref) {
+                if (!kSync && res.dref) {
                     if constexpr (kAnch) {
                         cp_async<8>(&s_hi[prv][wib][lane], anch_node(coords, ni) + 8 * ((fs >> 1) & 1), pol_keep);
                         cp_async<8>(&s_hj[prv][wib][lane], anch_node(coords, nj) + 8 * ((fs >> 2) & 1), pol_keep);
@@ -999,6 +1007,8 @@ const void* tiles_fn_t(int variant) {
         if (variant == 8) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false>);
         if (variant == 7 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true>);
         if (variant == 8 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true>);
+        if (variant == 9) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, true>);
+        if (variant == 9 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, true>);
     }
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
@@ -1014,7 +1024,7 @@ const void* tiles_fn(int variant, bool k32) {
 size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
-    if (variant == 7 || variant == 8)
+    if (variant == 7 || variant == 8 || variant == 9)
         return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0) +
                (PGL_LEAN_BULK ? 8 * 2 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
