@@ -36,6 +36,8 @@ KERNELS = [
     pytest.param(0, 7, 2, id="tiles-v7-anch"),
     pytest.param(0, 8, 1, id="tiles-v8-f64"),
     pytest.param(0, 8, 2, id="tiles-v8-anch"),
+    pytest.param(0, 9, 1, id="tiles-v9-f64"),
+    pytest.param(0, 9, 2, id="tiles-v9-anch"),
     pytest.param(1, 0, 1, id="iid-f64"),
     pytest.param(1, 0, 2, id="iid-anch"),
 ]
@@ -68,7 +70,7 @@ def test_device_accounting_config1(pgl, gpu, samp, variant, prec):
 @pytest.mark.parametrize("samp,variant,prec", KERNELS)
 @pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (2, 3), (4, 1)])
 def test_device_accounting_reuse(pgl, gpu, samp, variant, prec, drf, srf):
-    if variant in (7, 8):
+    if variant in (7, 8, 9):
         pytest.skip("the lean kernel covers drf 1 only (the host picks variant 6 for reuse runs)")
     g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
     st = pgl.RunStats()
@@ -166,6 +168,7 @@ def zipf_pmf(n, theta):
 
 SAMPLER_KERNELS = [pytest.param(0, 1, id="tiles-v1"), pytest.param(0, 6, id="tiles-v6"),
                    pytest.param(0, 7, id="tiles-v7"), pytest.param(0, 8, id="tiles-v8"),
+                   pytest.param(0, 9, id="tiles-v9"),
                    pytest.param(1, 0, id="iid")]
 
 
@@ -250,7 +253,7 @@ def test_outcome_frequencies_two_step_path(pgl, gpu, samp, variant):
     1/4 of its draws (two collisions on a two-step path). So P(applied) =
     9/16 for uniform selections and 3/4 for cooling ones, +-0.02. (The lean
     kernels need >= 32 steps: 64 disjoint two-step paths, same frequencies.)"""
-    n_paths, n_iters = (64, 200) if variant in (7, 8) else (1, 8000)
+    n_paths, n_iters = (64, 200) if variant in (7, 8, 9) else (1, 8000)
     g = pgl.build_graph([5] * (2 * n_paths), [[(2 * p, 0), (2 * p + 1, 0)] for p in range(n_paths)])
     d = pgl.LayoutDiag()
     pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters, global_seed=9),
@@ -277,6 +280,37 @@ def test_lean_kernel_preconditions(pgl, gpu):
                            ext=pgl.LayoutExt(**{"kernel_variant": 8, **ext}))
     with pytest.raises(pgl.InvalidParameter):
         pgl.run_layout_reuse(g, pgl.LayoutConfig(n_iters=2, drf=2, srf=2), ext=pgl.LayoutExt(kernel_variant=7))
+    # unit length / random order: a power of two, below 32 only with the random order, lean kernel only
+    for ext in [dict(kernel_variant=7, unit_len=3, unit_order=pgl.ORDER_RANDOM),
+                dict(kernel_variant=7, unit_len=8),
+                dict(kernel_variant=6, unit_order=pgl.ORDER_RANDOM),
+                dict(sampling=pgl.SAMPLING_IID, unit_order=pgl.ORDER_RANDOM)]:
+        with pytest.raises(pgl.InvalidParameter):
+            pgl.run_layout(g, pgl.LayoutConfig(n_iters=2), ext=pgl.LayoutExt(**ext))
+
+
+@pytest.mark.parametrize("variant", [7, 9])
+@pytest.mark.parametrize("unit_len", [1, 4, 32])
+def test_lean_random_units_visit_uniformly(pgl, gpu, variant, unit_len):
+    """PGL_ORDER_RANDOM with unit_len picks: every step's primary-visit count
+    is Binomial-like around N/S (no step range favoured: chi-square over 16
+    stretches of the step range), the device RunStats identities hold."""
+    g = pgl.generate_synthetic_pangenome(4, 3000, 4, 0.05)
+    S = g.total_steps()
+    d = pgl.LayoutDiag(total_steps=S)
+    st = pgl.RunStats()
+    n_iters = 200
+    pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters), stats=st,
+                   ext=pgl.LayoutExt(kernel_variant=variant, unit_order=pgl.ORDER_RANDOM, unit_len=unit_len,
+                                     pair_window=1, diag=d))
+    v = d.primary_visits.astype(np.float64)
+    assert v.sum() == n_iters * 10 * S == st.primary_steps
+    assert st.updates_applied + st.updates_skipped == st.updates_attempted
+    parts = np.array([p.sum() for p in np.array_split(v, 16)])
+    exp = np.array([len(p) for p in np.array_split(v, 16)]) * v.sum() / S
+    # unit starts are i.i.d.: counts of a stretch are sums of unit_len-step runs
+    chi2 = ((parts - exp) ** 2 / (exp * unit_len)).sum()
+    assert sst.chi2.sf(chi2, 15) > 1e-4, chi2
 
 
 @pytest.mark.parametrize("variant", [7, 8])
