@@ -52,8 +52,8 @@ def main():
                     help="reference scores computed elsewhere (tools/score_ref_layout.py lines or a previous "
                          "parity.py output): the reference layouts are not recomputed")
     args = ap.parse_args()
-    seeds = [int(s) for s in args.seeds.split(",")]
-    ref_seeds = [int(s) for s in (args.ref_seeds or args.seeds).split(",")]
+    seeds = [int(s) for s in args.seeds.split(",") if s]  # empty: score reference layouts only
+    ref_seeds = [int(s) for s in (args.ref_seeds or args.seeds).split(",") if s]
     R = Reference()
     t = time.time()
     gr = R.generate(*GEN[args.config])
@@ -106,6 +106,8 @@ def main():
             print("ref", res["ref"][-1], flush=True)
             flush()
     for key in ("sps_gpu_spn%d" % args.gpu_spn, "sps_ref_spn%d" % args.ref_spn):
+        if not res["gpu"] or not res["ref"]:
+            continue
         mg = statistics.median(r[key]["mean"] for r in res["gpu"])
         mr = statistics.median(r[key]["mean"] for r in res["ref"])
         res["ratio_" + key] = mg / mr
