@@ -17,7 +17,7 @@ g = (P.generate_nested_pangenome(5, 200000, 500, 3, 0.05) if name == "c5"
      else P.generate_synthetic_pangenome(*GEN[name]))
 dg = P.DeviceGraph(g)
 upd = 30 * 10 * g.total_steps()
-ext = P.LayoutExt(coord_precision=prec, kernel_variant=variant, **extra)
+ext = P.LayoutExt(**{"coord_precision": prec, "kernel_variant": variant, **extra})
 kw = {"zipf_space_max": 100000} if name == "c5" else {}
 dg.layout(P.LayoutConfig(n_iters=3, **kw), ext=ext, copy_out=False)
 out = []
