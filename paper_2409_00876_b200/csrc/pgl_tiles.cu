@@ -872,8 +872,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
     // Round t: apply unit t-2, resolve unit t-1, select unit t. Each round
     // commits two groups (endpoint copies of t-1, then record copies of t):
     // apply(t-2) waits for all but the newest group, resolve(t-1) for all.
-    for (uint32_t t = 0; t < N + 2; ++t) {
-        const int cur = t & 1, prv = cur ^ 1;
+    // one round as a lambda over a compile-time slot (t & 1), the loop
+    // unrolled by two: the slot offsets fold into the addresses
+    auto round = [&](uint32_t t, auto slot) {
+        constexpr int cur = decltype(slot)::value, prv = cur ^ 1;
         if (t >= 2) {  // 1. apply unit t-2 (endpoint slot (t-2)&1 = cur)
             cp_async_wait<1>();
             const LeanRes res = s_res[cur][wib][lane];
@@ -964,7 +966,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         }
         cp_async_commit();
         __syncwarp();
+    };
+    uint32_t t = 0;
+    for (; t + 1 < N + 2; t += 2) {
+        round(t, std::integral_constant<int, 0>{});
+        round(t + 1, std::integral_constant<int, 1>{});
     }
+    if (t < N + 2) round(t, std::integral_constant<int, 0>{});
 
     if constexpr (kSmemRng) {
         rng.s0[tid] = r.s[0];
