@@ -464,6 +464,10 @@ __device__ __forceinline__ void tma_load_hint(void* dst, const void* src, uint32
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
         :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(p));
+}
+
 // generic-proxy accesses of shared memory before a later async-proxy write
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

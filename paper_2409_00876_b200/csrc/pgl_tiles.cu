@@ -669,6 +669,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 //     slots instead of 3, and the resolved update is 16 bytes (32-bit d_ref);
 //     with 64 registers and 56 KB of shared memory per 256-thread CTA, four
 //     CTAs fit an SM (variant 8) instead of three.
+#ifndef PGL_LEAN_SYNC_PREFETCH
+#define PGL_LEAN_SYNC_PREFETCH 1  // variant 9: L2 prefetch of the endpoints a round ahead
+#endif
 #ifndef PGL_LEAN_BULK
 #define PGL_LEAN_BULK 0  // 1: unit records staged by one cp.async.bulk (TMA) per warp round (C3: 49.9 vs 52.9 G upd/s with lane cp.async)
 #endif
@@ -924,6 +927,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const uint32_t ni = wi[0], nj = wj[0];
                 const uint32_t pi = wi[(fs & 2u) ? 2 : 1], pj = wj[(fs & 4u) ? 2 : 1];  // pe_lo : ps_lo
                 res = LeanRes{ni, nj, fs, pi > pj ? pi - pj : pj - pi};
+                if (kSync && PGL_LEAN_SYNC_PREFETCH && res.dref) {
+                    // synchronous apply next round: pull the endpoints' lines
+                    // into L2 now (no registers, no shared-memory write)
+                    prefetch_l2(Coord<T>::copy_src(coords, ni, (fs >> 1) & 1));
+                    prefetch_l2(Coord<T>::copy_src(coords, nj, (fs >> 2) & 1));
+                }
                 if (!kSync && res.dref) {
                     if constexpr (kAnch) {
                         cp_async<8>(&s_hi[prv][wib][lane], anch_node(coords, ni) + 8 * ((fs >> 1) & 1), pol_keep);
@@ -1017,6 +1026,8 @@ const void* tiles_fn_t(int variant) {
         if (variant == 8 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true>);
         if (variant == 9) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, true>);
         if (variant == 9 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, true>);
+        if (variant == 10) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false, true>);
+        if (variant == 10 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, true>);
     }
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
@@ -1032,7 +1043,7 @@ const void* tiles_fn(int variant, bool k32) {
 size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
-    if (variant == 7 || variant == 8 || variant == 9)
+    if (variant >= 7 && variant <= 10)
         return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0) +
                (PGL_LEAN_BULK ? 8 * 2 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
