@@ -732,13 +732,13 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
         // cap binds hard (config 1)
         v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 7 : 6) : 1;
     }
-    if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 10))
-        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-10");
-    if (v >= 7 && v <= 10 && (!lean_ok || force64))
+    if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 12))
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-12");
+    if (v >= 7 && v <= 12 && (!lean_ok || force64))
         raise(PGL_ERR_INVALID_PARAMETER,
-              "pgl_layout_ext.kernel_variant 7-10 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
+              "pgl_layout_ext.kernel_variant 7-12 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
               "pair_window 1 or 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
-    return v | force64 | (v >= 7 && v <= 10 && ext.diag ? 32 : 0);
+    return v | force64 | (v >= 7 && v <= 12 && ext.diag ? 32 : 0);
 }
 
 uint32_t auto_max_warps(uint64_t n_nodes) {
@@ -963,7 +963,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         if (ext.unit_order == PGL_ORDER_RANDOM &&
-            (ext.sampling != PGL_SAMPLING_TILES || (shape.variant & 15) < 7 || (shape.variant & 15) > 10))
+            (ext.sampling != PGL_SAMPLING_TILES || (shape.variant & 15) < 7 || (shape.variant & 15) > 12))
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the random order needs the lean tile kernel "
                                              "(kernel_variant 7 or 8)");
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -1039,7 +1039,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         a.n_warps = n_warps;
         a.units = (spi + 31) / 32;
         const bool lean = !replay && ext.sampling == PGL_SAMPLING_TILES &&
-                          ((shape.variant & 15) >= 7 && (shape.variant & 15) <= 10);
+                          ((shape.variant & 15) >= 7 && (shape.variant & 15) <= 12);
         a.units_full = spi / 32;
         a.tail_n = static_cast<uint32_t>(spi % 32);
         {   // unit order of k_sgd_tiles: u = (a*k + b) mod U, gcd(a, U) = 1,

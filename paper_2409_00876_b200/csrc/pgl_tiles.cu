@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_tiles(DevGraph g, void*
 //     with 64 registers and 56 KB of shared memory per 256-thread CTA, four
 //     CTAs fit an SM (variant 8) instead of three.
 #ifndef PGL_LEAN_SYNC_PREFETCH
-#define PGL_LEAN_SYNC_PREFETCH 1  // variant 9: L2 prefetch of the endpoints a round ahead
+#define PGL_LEAN_SYNC_PREFETCH 0  // 1: variants 9/10 prefetch the endpoints into L2 a round ahead (C3: 56.3 vs 58.1 G upd/s without)
 #endif
 #ifndef PGL_LEAN_BULK
 #define PGL_LEAN_BULK 0  // 1: unit records staged by one cp.async.bulk (TMA) per warp round (C3: 49.9 vs 52.9 G upd/s with lane cp.async)
@@ -700,7 +700,10 @@ __host__ __device__ constexpr size_t lean_smem_bytes(bool anchored) {
 // kSync (variant 9): the endpoints are not staged a round ahead; apply reads
 // them from L2 and writes them back at once -- a read-to-write window of one
 // L2 round trip, as the i.i.d. kernel has (the staged window is a full round).
-template <typename T, int kMinBlocks, bool kDiag, bool kSync = false>
+// kSync 2 (variants 11, 12): the same loads issued at the start of the
+// round and consumed after the round's resolve and select, which hide their
+// latency (window: one round's integer work, no shared-memory staging).
+template <typename T, int kMinBlocks, bool kDiag, int kSync = 0>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                DevStats* stats, IterArgs a) {
     const uint32_t tid = blockIdx.x * 256u + threadIdx.x;
@@ -879,7 +882,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
     // unrolled by two: the slot offsets fold into the addresses
     auto round = [&](uint32_t t, auto slot) {
         constexpr int cur = decltype(slot)::value, prv = cur ^ 1;
-        if (t >= 2) {  // 1. apply unit t-2 (endpoint slot (t-2)&1 = cur)
+        // kSync 2: unit t-2's endpoint loads go out first, its update comes last
+        [[maybe_unused]] LeanRes early{0, 0, 0, 0};
+        [[maybe_unused]] double evix = 0, eviy = 0, evjx = 0, evjy = 0;
+        if (kSync == 2 && t >= 2) {
+            early = s_res[cur][wib][lane];
+            const bool live = (early.flags & 1u) && early.dref != 0;
+            primary += (early.flags >> 4) & 1u;
+            skipped += ((early.flags & 16u) && !live) ? 1u : 0u;
+            if constexpr (kDiag)
+                if (early.flags & 16u) diag_outcome(a, early.flags & 32u, live);
+            if (live) {
+                CoordHint<T>::get(coords, early.ni, (early.flags >> 1) & 1, pol_keep, evix, eviy);
+                CoordHint<T>::get(coords, early.nj, (early.flags >> 2) & 1, pol_keep, evjx, evjy);
+            } else {
+                early.flags = 0;
+            }
+        }
+        if (kSync != 2 && t >= 2) {  // 1. apply unit t-2 (endpoint slot (t-2)&1 = cur)
             cp_async_wait<1>();
             const LeanRes res = s_res[cur][wib][lane];
             const bool live = (res.flags & 1u) && res.dref != 0;
@@ -891,7 +911,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const int ei = (res.flags >> 1) & 1, ej = (res.flags >> 2) & 1;
                 double vix, viy, vjx, vjy;
                 const double d = static_cast<double>(res.dref);
-                if constexpr (kSync) {
+                if constexpr (kSync == 1) {
                     CoordHint<T>::get(coords, res.ni, ei, pol_keep, vix, viy);
                     CoordHint<T>::get(coords, res.nj, ej, pol_keep, vjx, vjy);
                     applied += hog_apply_io_t<T>(coords, res.ni, ei, res.nj, ej, d, a.eta, r, pol_keep, vix, viy, vjx,
@@ -927,13 +947,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 const uint32_t ni = wi[0], nj = wj[0];
                 const uint32_t pi = wi[(fs & 2u) ? 2 : 1], pj = wj[(fs & 4u) ? 2 : 1];  // pe_lo : ps_lo
                 res = LeanRes{ni, nj, fs, pi > pj ? pi - pj : pj - pi};
-                if (kSync && PGL_LEAN_SYNC_PREFETCH && res.dref) {
+                if (kSync == 1 && PGL_LEAN_SYNC_PREFETCH && res.dref) {
                     // synchronous apply next round: pull the endpoints' lines
                     // into L2 now (no registers, no shared-memory write)
                     prefetch_l2(Coord<T>::copy_src(coords, ni, (fs >> 1) & 1));
                     prefetch_l2(Coord<T>::copy_src(coords, nj, (fs >> 2) & 1));
                 }
-                if (!kSync && res.dref) {
+                if (kSync == 0 && res.dref) {
                     if constexpr (kAnch) {
                         cp_async<8>(&s_hi[prv][wib][lane], anch_node(coords, ni) + 8 * ((fs >> 1) & 1), pol_keep);
                         cp_async<8>(&s_hj[prv][wib][lane], anch_node(coords, nj) + 8 * ((fs >> 2) & 1), pol_keep);
@@ -972,6 +992,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 i0 = static_cast<uint32_t>(__umul64hi(z ^ (z >> 31), S));
             }
             s_res[cur][wib][lane].flags = select(s_ri[cur][wib], s_rj[cur][wib]);  // slot free: unit t-2 applied
+        }
+        if (kSync == 2 && (early.flags & 1u)) {  // unit t-2's update, its endpoints loaded at the round's start
+            applied += hog_apply_io_t<T>(coords, early.ni, (early.flags >> 1) & 1, early.nj, (early.flags >> 2) & 1,
+                                         static_cast<double>(early.dref), a.eta, r, pol_keep, evix, eviy, evjx, evjy);
         }
         cp_async_commit();
         __syncwarp();
@@ -1024,10 +1048,14 @@ const void* tiles_fn_t(int variant) {
         if (variant == 8) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false>);
         if (variant == 7 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true>);
         if (variant == 8 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true>);
-        if (variant == 9) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, true>);
-        if (variant == 9 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, true>);
-        if (variant == 10) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false, true>);
-        if (variant == 10 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, true>);
+        if (variant == 9) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, 1>);
+        if (variant == 9 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, 1>);
+        if (variant == 10) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false, 1>);
+        if (variant == 10 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, 1>);
+        if (variant == 11) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, 2>);
+        if (variant == 11 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, 2>);
+        if (variant == 12) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false, 2>);
+        if (variant == 12 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, 2>);
     }
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
@@ -1043,7 +1071,7 @@ const void* tiles_fn(int variant, bool k32) {
 size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
-    if (variant >= 7 && variant <= 10)
+    if (variant >= 7 && variant <= 12)
         return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0) +
                (PGL_LEAN_BULK ? 8 * 2 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
