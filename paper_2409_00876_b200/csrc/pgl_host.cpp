@@ -727,10 +727,12 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
         PGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         // the async pipeline once the cap allows a CTA's worth of warps per
         // SM (config 5, cap 2988 warps: 38.7 vs 36.1 G upd/s for variant 1,
-        // at lower SPS) -- its lean specialisation where the run allows;
+        // at lower SPS) -- its lean specialisation where the run allows, with
+        // synchronous apply at 4 CTAs/SM (variant 10: C3 58.0 vs 53.6 G upd/s
+        // for the staged variant 7, profiles/r02_ab_sync_early.jsonl);
         // the register pipeline's shorter read-to-write window where the
         // cap binds hard (config 1)
-        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 7 : 6) : 1;
+        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 10 : 6) : 1;
     }
     if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 12))
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-12");
