@@ -215,14 +215,25 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config: str, coord: str):
+def kernel_name(variant: int) -> str:
+    """The SGD kernel a layout ran (pgl_timing.kernel_variant: 0 = the
+    i.i.d. kernel, 7-12 the lean tile kernel, else the general tile kernel)."""
+    return "k_sgd_hogwild" if variant == 0 else ("k_sgd_lean" if 7 <= variant <= 12 else "k_sgd_tiles")
+
+
+def ncu_key(config: str, coord: str, variant: int) -> str:
+    """profiles/ncu_traffic.json key of a capture of this kernel on this config."""
+    return f"{config}_{coord}" + ("_iid" if variant == 0 else "")
+
+
+def ncu_traffic(config: str, coord: str, variant: int = 10):
     """(dram bytes per SGD launch, ncu ms of that launch, cache/sector
     summary) from the committed ncu --set full capture
     (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            e = json.load(f)[f"{config}_{coord}"]
+            e = json.load(f)[ncu_key(config, coord, variant)]
     except (OSError, KeyError, ValueError):
         return None, None, None
     keys = ("l2_hit_pct", "l1_hit_pct", "ld_bytes_per_sector", "st_bytes_per_sector", "lsu_sectors_per_update",
@@ -495,7 +506,7 @@ def run_ours(args, dist: Dist):
     payload = BYTES_PER_UPDATE[args.coord]
     per_launch = (10 * S // cfg.srf) * cfg.drf
     payload_gbs = per_launch * payload / (sgd_launch_ms / 1e3) / 1e9
-    traffic, ncu_ms, ncu_cache = ncu_traffic(args.config, args.coord)
+    traffic, ncu_ms, ncu_cache = ncu_traffic(args.config, args.coord, timing.variant)
     if traffic:
         achieved, model = traffic / (sgd_launch_ms / 1e3) / 1e9, "ncu-measured DRAM bytes per launch / live launch time"
     else:
@@ -522,7 +533,7 @@ def run_ours(args, dist: Dist):
                     "bytes": "pgl_transfer_bytes deltas around the timed calls"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_sgd_lean" if timing.variant in (7, 8) else "k_sgd_tiles",
+                         "kernel": kernel_name(timing.variant),
                          "kernel_variant": timing.variant,
                          "model": model, "launch_ms": sgd_launch_ms, "ncu_launch_ms": ncu_ms,
                          "payload": {"bytes_per_update": payload, "achieved": payload_gbs,
