@@ -782,6 +782,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
                                 ext.hop_lanes || ext.reuse_shuffle;
         ext.sampling = tile_knobs || cap >= static_cast<uint32_t>(sms) * 24 ? PGL_SAMPLING_TILES : PGL_SAMPLING_IID;
     }
+    if (ext.mode == PGL_MODE_HOGWILD && ext.sampling == PGL_SAMPLING_IID && ext.kernel_variant > 7)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: i.i.d. kernel variants are 0-7");
     if (ext.reuse_shuffle && (ext.mode != PGL_MODE_HOGWILD || ext.sampling != PGL_SAMPLING_TILES))
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle needs the Hogwild tile sampler");
     if (ext.reuse_shuffle && G->n_paths >= (1u << 19))

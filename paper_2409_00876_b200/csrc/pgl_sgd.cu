@@ -49,13 +49,24 @@ struct Sel {
 // Stage A (warp-uniform call): the batch decision of engine.cpp:115-124 for
 // this round, then select_step_pair (:52-80) and the two endpoint coins, and
 // issue the two step-record gathers. Nothing waits on the gathers here.
+// `bpos` is base % batch, advanced here by one round (no 64-bit modulo per
+// lane and round).
 template <bool kActiveCheck>
 __device__ __forceinline__ Sel stage_select(const DevGraph& g, Xo& r, const IterArgs& a, uint64_t base,
                                             uint64_t count, uint32_t lane, bool& carry, uint32_t& b_first,
-                                            uint32_t& b_first_cool, uint32_t& b_second, uint64_t pol_stream) {
+                                            uint32_t& b_first_cool, uint32_t& b_second, uint64_t pol_stream,
+                                            uint32_t& bpos) {
     const uint64_t s = base + lane;
     const bool active = s < count;
-    const uint64_t in_batch = s % a.batch;
+    uint32_t in_batch = bpos + lane;
+    if (a.batch >= 32) {
+        if (in_batch >= a.batch) in_batch -= a.batch;
+        bpos += 32;
+        if (bpos >= a.batch) bpos -= a.batch;
+    } else {
+        in_batch %= a.batch;
+        bpos = (bpos + 32) % a.batch;
+    }
     bool mine = false;
     if (active && in_batch == 0) {
         if (a.force_cooling) {
@@ -154,9 +165,18 @@ __device__ __forceinline__ uint32_t stage_update(const Sel& sel, void* coords, X
     return applied;
 }
 
-template <typename T, int kMinBlocks>
+// kDepth: rounds in flight per warp. Round r's step records are gathered
+// while rounds r-kDepth+1 .. r-1 update; the records are read-only, so a
+// deeper record pipeline adds memory-level parallelism without widening any
+// coordinate's read-to-write window (each update still reads its endpoints
+// and writes them back in one stage, as apply_endpoint_update does).
+// kPrefetch: while round r updates, the endpoint lines of round r+1 (whose
+// records arrived a round earlier) are pulled into L2 -- no registers, no
+// read of the values, so no update sees an older coordinate than without.
+template <typename T, int kMinBlocks, int kDepth, bool kPrefetch = false>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                      DevStats* stats, IterArgs a) {
+    static_assert(kDepth >= 2 && kDepth <= 4, "pipeline depth");
     const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint32_t warp = static_cast<uint32_t>(tid >> 5);
     const uint32_t lane = threadIdx.x & 31;
@@ -170,17 +190,34 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_hogwild(DevGraph g, voi
 
     uint32_t applied = 0, b_first = 0, b_first_cool = 0, b_second = 0, primary = 0, skipped = 0;
     bool carry = false;
-    // Two-stage software pipeline over rounds: the step records of round
-    // r+1 are in flight while round r gathers and updates coordinates.
-    Sel cur = stage_select<true>(g, r, a, 0, count, lane, carry, b_first, b_first_cool, b_second, pol_stream);
+    uint32_t bpos = 0;
+    // Software pipeline over rounds: the step records of the next kDepth-1
+    // rounds are in flight while this round gathers and updates coordinates.
+    Sel q[kDepth - 1];
+#pragma unroll
+    for (int d = 0; d < kDepth - 1; ++d) {
+        q[d].flags = 0;
+        if (static_cast<uint64_t>(d) * 32 < count)
+            q[d] = stage_select<true>(g, r, a, static_cast<uint64_t>(d) * 32, count, lane, carry, b_first,
+                                      b_first_cool, b_second, pol_stream, bpos);
+    }
     for (uint64_t base = 0; base < count; base += 32) {
         Sel nxt;
         nxt.flags = 0;
-        if (base + 32 < count)
-            nxt = stage_select<true>(g, r, a, base + 32, count, lane, carry, b_first, b_first_cool, b_second,
-                                     pol_stream);
-        applied += stage_update<T>(cur, coords, r, a, pol_keep, primary, skipped);
-        cur = nxt;
+        const uint64_t ahead = base + static_cast<uint64_t>(kDepth - 1) * 32;
+        if (ahead < count)
+            nxt = stage_select<true>(g, r, a, ahead, count, lane, carry, b_first, b_first_cool, b_second,
+                                     pol_stream, bpos);
+        if constexpr (kPrefetch && kDepth >= 3) {
+            if (q[1].flags & 1u) {
+                prefetch_l2(Coord<T>::copy_src(coords, q[1].ri.node, (q[1].flags >> 1) & 1));
+                prefetch_l2(Coord<T>::copy_src(coords, q[1].rj.node, (q[1].flags >> 2) & 1));
+            }
+        }
+        applied += stage_update<T>(q[0], coords, r, a, pol_keep, primary, skipped);
+#pragma unroll
+        for (int d = 0; d + 1 < kDepth - 1; ++d) q[d] = q[d + 1];
+        q[kDepth - 2] = nxt;
     }
 
     rng.s0[tid] = r.a;
@@ -211,11 +248,23 @@ __global__ void k_f32_to_f64(const float* __restrict__ s, double* __restrict__ d
 
 }  // namespace
 
-// Kernel variants: occupancy target 2 blocks/SM (no spills) or 3 (80 regs).
+// Kernel variants (pgl_layout_ext.kernel_variant with PGL_SAMPLING_IID):
+// bit 0 = occupancy target 3 blocks/SM (80 registers) instead of 2 (no
+// spills); variant >> 1 = extra rounds of step records in flight (depth 2,
+// 3 or 4); 6 / 7 = depth 3 / 4 with the next round's endpoints prefetched
+// into L2.
 template <typename T>
 const void* hogwild_fn(int variant) {
-    return variant == 1 ? reinterpret_cast<const void*>(k_sgd_hogwild<T, 3>)
-                        : reinterpret_cast<const void*>(k_sgd_hogwild<T, 1>);
+    switch (variant) {
+        case 1: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 3, 2>);
+        case 2: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 1, 3>);
+        case 3: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 3, 3>);
+        case 4: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 1, 4>);
+        case 5: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 3, 4>);
+        case 6: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 1, 3, true>);
+        case 7: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 1, 4, true>);
+        default: return reinterpret_cast<const void*>(k_sgd_hogwild<T, 1, 2>);
+    }
 }
 
 const void* hogwild_fn_kind(int coord_kind, int variant) {

@@ -226,17 +226,23 @@ def test_hogwild_switch_point(pgl, gpu, n_iters, samp):
     assert st.batches_first_half == n_iters * spi - (n_iters // 2) * spi
 
 
-def test_hogwild_batches_count_per_warp(pgl, gpu):
-    """batch_size 32, i.i.d. sampler: every warp's share opens ceil(share/32) batches."""
+@pytest.mark.parametrize("batch", [1, 7, 32, 48, 100])
+@pytest.mark.parametrize("variant", [0, 2, 4, 5])
+def test_hogwild_batches_count_per_warp(pgl, gpu, batch, variant):
+    """i.i.d. sampler, every pipeline depth: each warp's share of the
+    iteration's picks opens ceil(share/batch) batches (engine.cpp:115-124
+    per worker), the cooling coin drawn once per batch."""
     g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
     st = pgl.RunStats()
     with pgl.DeviceGraph(g) as dg:
-        dg.layout(pgl.LayoutConfig(n_iters=2), stats=st, ext=pgl.LayoutExt(sampling=pgl.SAMPLING_IID))
+        dg.layout(pgl.LayoutConfig(n_iters=2, batch_size=batch), stats=st,
+                  ext=pgl.LayoutExt(sampling=pgl.SAMPLING_IID, kernel_variant=variant))
         warps = dg.timing().device_threads // 32
     spi = 10 * g.total_steps()
     share, rem = divmod(spi, warps)
-    per_iter = rem * -(-(share + 1) // 32) + (warps - rem) * -(-share // 32)
+    per_iter = rem * -(-(share + 1) // batch) + (warps - rem) * -(-share // batch)
     assert st.batches_first_half == per_iter and st.batches_second_half == per_iter
+    assert st.primary_steps == 2 * spi
 
 
 def test_tiles_batches_per_unit(pgl, gpu):

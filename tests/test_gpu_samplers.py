@@ -40,6 +40,9 @@ KERNELS = [
     pytest.param(0, 9, 2, id="tiles-v9-anch"),
     pytest.param(1, 0, 1, id="iid-f64"),
     pytest.param(1, 0, 2, id="iid-anch"),
+    pytest.param(1, 2, 1, id="iid-d3-f64"),
+    pytest.param(1, 4, 2, id="iid-d4-anch"),
+    pytest.param(1, 5, 1, id="iid-d4-3cta-f64"),
 ]
 
 
