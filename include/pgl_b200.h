@@ -178,11 +178,15 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t kernel_variant;  /* tile kernel: 0 = auto (6 once the concurrency cap allows
-                                 8 warps per SM, else 1); 1 = register pipeline, 2 CTAs/SM;
-                                 2 = register pipeline, 3 CTAs/SM; 5/6 = cp.async pipeline
-                                 via shared memory, 4/3 CTAs/SM.
-                                 i.i.d. kernel: 0 = 2 CTAs/SM, 1 = 3 CTAs/SM */
+    uint32_t kernel_variant;  /* tile kernel: 0 = auto (10 for LayoutConfig{}-shaped runs once
+                                 the concurrency cap allows full residency, 6 for the general
+                                 case, 1 where the cap binds); 1/2 = register pipeline, 2/3
+                                 CTAs/SM; 5/6 = cp.async pipeline via shared memory, 4/3
+                                 CTAs/SM; 7-12 = the lean kernel (pgl_tiles.cu).
+                                 i.i.d. kernel (PGL_SAMPLING_IID): 0 = auto; 8 = two-stage,
+                                 2 CTAs/SM; 1-5: bit 0 = 3 CTAs/SM, variant >> 1 = rounds of
+                                 step records in flight beyond the current one (depth 2-4);
+                                 6/7 = depth 3/4 + next round's endpoints prefetched to L2 */
     uint32_t l2_fetch_bytes;  /* cudaLimitMaxL2FetchGranularity during the layout; 0 = 32 */
     uint32_t sampling;        /* pgl_sampling (Hogwild mode only; default PGL_SAMPLING_AUTO) */
     uint32_t unit_order;      /* pgl_unit_order (tile sampling only) */

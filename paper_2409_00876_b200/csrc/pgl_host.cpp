@@ -743,6 +743,10 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
     return v | force64 | (v >= 7 && v <= 12 && ext.diag ? 32 : 0);
 }
 
+// The i.i.d. kernel's variant when pgl_layout_ext.kernel_variant is 0
+// (pgl_sgd.cu hogwild_fn).
+constexpr int kIidAutoVariant = 8;
+
 uint32_t auto_max_warps(uint64_t n_nodes) {
     // Hogwild concurrency cap: keep the number of in-flight updates well
     // below the number of endpoints so concurrent read-modify-writes on one
@@ -782,8 +786,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
                                 ext.hop_lanes || ext.reuse_shuffle;
         ext.sampling = tile_knobs || cap >= static_cast<uint32_t>(sms) * 24 ? PGL_SAMPLING_TILES : PGL_SAMPLING_IID;
     }
-    if (ext.mode == PGL_MODE_HOGWILD && ext.sampling == PGL_SAMPLING_IID && ext.kernel_variant > 7)
-        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: i.i.d. kernel variants are 0-7");
+    if (ext.mode == PGL_MODE_HOGWILD && ext.sampling == PGL_SAMPLING_IID && ext.kernel_variant > 8)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: i.i.d. kernel variants are 0-8");
     if (ext.reuse_shuffle && (ext.mode != PGL_MODE_HOGWILD || ext.sampling != PGL_SAMPLING_TILES))
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.reuse_shuffle needs the Hogwild tile sampler");
     if (ext.reuse_shuffle && G->n_paths >= (1u << 19))
@@ -961,7 +965,8 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     if (!replay) {
         const uint32_t cap = ext.max_warps ? ext.max_warps : auto_max_warps(V);
         shape = ext.sampling == PGL_SAMPLING_IID
-                    ? sgd_shape(G->device, kind, cap, static_cast<int>(ext.block_threads), static_cast<int>(ext.kernel_variant))
+                    ? sgd_shape(G->device, kind, cap, static_cast<int>(ext.block_threads),
+                                ext.kernel_variant ? static_cast<int>(ext.kernel_variant) : kIidAutoVariant)
                     : tiles_shape(G->device, kind, cap, static_cast<int>(ext.block_threads),
                                   tile_variant(G->device, ext, cap, lean_ok), G->sum.total_steps);
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;

@@ -248,10 +248,11 @@ __global__ void k_f32_to_f64(const float* __restrict__ s, double* __restrict__ d
 
 }  // namespace
 
-// Kernel variants (pgl_layout_ext.kernel_variant with PGL_SAMPLING_IID):
-// bit 0 = occupancy target 3 blocks/SM (80 registers) instead of 2 (no
-// spills); variant >> 1 = extra rounds of step records in flight (depth 2,
-// 3 or 4); 6 / 7 = depth 3 / 4 with the next round's endpoints prefetched
+// Kernel variants (pgl_layout_ext.kernel_variant with PGL_SAMPLING_IID; 0 =
+// the host's auto choice): 8 = depth 2, 2 blocks/SM (the round-1 kernel);
+// 1-5: bit 0 = occupancy target 3 blocks/SM (80 registers, spills) instead
+// of 2, variant >> 1 = extra rounds of step records in flight (depth 2, 3
+// or 4); 6 / 7 = depth 3 / 4 with the next round's endpoints prefetched
 // into L2.
 template <typename T>
 const void* hogwild_fn(int variant) {

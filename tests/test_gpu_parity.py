@@ -227,7 +227,7 @@ def test_hogwild_switch_point(pgl, gpu, n_iters, samp):
 
 
 @pytest.mark.parametrize("batch", [1, 7, 32, 48, 100])
-@pytest.mark.parametrize("variant", [0, 2, 4, 5])
+@pytest.mark.parametrize("variant", [0, 8, 2, 4, 5, 7])
 def test_hogwild_batches_count_per_warp(pgl, gpu, batch, variant):
     """i.i.d. sampler, every pipeline depth: each warp's share of the
     iteration's picks opens ceil(share/batch) batches (engine.cpp:115-124

@@ -43,6 +43,8 @@ KERNELS = [
     pytest.param(1, 2, 1, id="iid-d3-f64"),
     pytest.param(1, 4, 2, id="iid-d4-anch"),
     pytest.param(1, 5, 1, id="iid-d4-3cta-f64"),
+    pytest.param(1, 7, 2, id="iid-d4pf-anch"),
+    pytest.param(1, 8, 1, id="iid-d2-f64"),
 ]
 
 

@@ -19,7 +19,10 @@ Each prints and appends one JSON line (per-seed values, medians, ratio to the
 reference median) to --out; the reference line comes first.
 
 usage: python tools/sampler_quality.py CONFIG --out F.jsonl [--variants ...]
-       [--seeds 101,...] [--cache DIR] [--ref-only]"""
+       [--seeds 101,...] [--cache DIR] [--ref-only] [--ref-json F]
+--ref-json: reference per-seed scores from a committed file (the "reference"
+object of profiles/r02_parity_c5.json, or a reference line of this tool's
+output) instead of laying the reference out again."""
 import argparse
 import json
 import os
@@ -63,6 +66,7 @@ def main():
     ap.add_argument("--seeds", default="101,102,103,104,105")
     ap.add_argument("--cache", default=None, help="directory for reference layouts (.npy)")
     ap.add_argument("--ref-only", action="store_true")
+    ap.add_argument("--ref-json", default=None)
     args = ap.parse_args()
     gen, gargs, over, threads, ref_spn, gpu_spn = CONFIGS[args.config]
     threads = threads or os.cpu_count()
@@ -84,7 +88,16 @@ def main():
             f.write(json.dumps(line) + "\n")
 
     ref = []
-    for s in seeds:
+    if args.ref_json:
+        with open(args.ref_json) as f:
+            txt = f.read().strip()
+        try:
+            doc = json.loads(txt)
+            doc = doc.get("reference", doc)
+        except ValueError:  # JSON lines: the first reference line
+            doc = next(json.loads(x) for x in txt.splitlines() if '"reference"' in x)
+        ref = [r for r in doc["per_seed"] if r["seed"] in seeds]
+    for s in ([] if args.ref_json else seeds):
         path = os.path.join(args.cache, f"{args.config}_ref_{s}.npy") if args.cache else None
         secs = None
         if path and os.path.exists(path):
@@ -99,7 +112,7 @@ def main():
         r = score(lay)
         r.update(seed=s, layout_s=secs, threads=threads)
         ref.append(r)
-    line = {"config": args.config, "variant": "reference", "per_seed": ref,
+    line = {"config": args.config, "variant": "reference", "per_seed": ref, "source": args.ref_json or "computed",
             "median_ref_est": statistics.median(r["ref_est"] for r in ref)}
     if gpu_spn:
         line["median_gpu_est"] = statistics.median(r["gpu_est"] for r in ref)
