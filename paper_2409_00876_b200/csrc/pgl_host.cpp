@@ -759,9 +759,46 @@ uint32_t auto_max_warps(uint64_t n_nodes) {
     return static_cast<uint32_t>(std::max<uint64_t>(4, std::min<uint64_t>(w, 1u << 24)));
 }
 
+// Device -> pageable host copy of a large result through two recycled
+// pinned chunks: the DMA of chunk c+1 overlaps the host threads' copy of
+// chunk c out of pinned memory (and the page faults of a fresh destination
+// are taken by all host threads instead of the driver's single staging
+// thread).
+void copy_out_staged(void* dst, const void* src, uint64_t bytes, cudaStream_t stream) {
+    constexpr uint64_t kChunk = 32ULL << 20;
+    if (bytes <= 2 * kChunk) {
+        PGL_CUDA(copy_async(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+        PGL_CUDA(cudaStreamSynchronize(stream));
+        return;
+    }
+    PinnedBuf pin;
+    pin.alloc(2 * kChunk);
+    char* bufs[2] = {static_cast<char*>(pin.p), static_cast<char*>(pin.p) + kChunk};
+    cudaEvent_t done[2];
+    PGL_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
+    PGL_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
+    const uint64_t n = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](uint64_t c) {
+        const uint64_t o = c * kChunk, b = std::min(kChunk, bytes - o);
+        PGL_CUDA(copy_async(bufs[c & 1], static_cast<const char*>(src) + o, b, cudaMemcpyDeviceToHost, stream));
+        PGL_CUDA(cudaEventRecord(done[c & 1], stream));
+    };
+    issue(0);
+    for (uint64_t c = 0; c < n; ++c) {
+        if (c + 1 < n) issue(c + 1);
+        PGL_CUDA(cudaEventSynchronize(done[c & 1]));
+        const uint64_t o = c * kChunk, b = std::min(kChunk, bytes - o);
+        const char* from = bufs[c & 1];
+        char* to = static_cast<char*>(dst) + o;
+        parallel_for(b, [&](uint64_t lo, uint64_t hi) { std::memcpy(to + lo, from + lo, hi - lo); });
+    }
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+}
+
 void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_ext* extp, int reuse,
                   pgl_iteration_cb cb, int cb_wants_coords, void* user, double* out_coords,
-                  pgl_run_stats* stats_out) {
+                  pgl_run_stats* stats_out, const double* pre_init) {
     const double t_call = now_s();
     if (!cfgp) raise(PGL_ERR_INVALID_PARAMETER, "config is null");
     const pgl_layout_config cfg = *cfgp;
@@ -850,9 +887,12 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
 
     // init_layout on the host (bit-exact), upload, narrow to FP32 on device.
     const double t_init = now_s();
-    G->pin.alloc(std::max<size_t>(G->pin.bytes, 4 * V * sizeof(double)));
-    double* hinit = static_cast<double*>(G->pin.p);
-    init_layout(&hv, G->sum.total_nt, cfg.global_seed, hinit);
+    const double* hinit = pre_init;  // pgl_layout_run computes it beside the graph upload
+    if (!hinit) {
+        G->pin.alloc(std::max<size_t>(G->pin.bytes, 4 * V * sizeof(double)));
+        init_layout(&hv, G->sum.total_nt, cfg.global_seed, static_cast<double*>(G->pin.p));
+        hinit = static_cast<const double*>(G->pin.p);
+    }
     G->coords64.alloc(4 * V);
     cudaEvent_t ev_begin, ev_end;
     PGL_CUDA(cudaEventCreate(&ev_begin));
@@ -1177,9 +1217,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     }
     if (out_coords) {
         to_f64(G, kind);
-        PGL_CUDA(copy_async(out_coords, G->coords64.p, 4 * V * sizeof(double), cudaMemcpyDeviceToHost,
-                                 G->stream));
-        PGL_CUDA(cudaStreamSynchronize(G->stream));
+        copy_out_staged(out_coords, G->coords64.p, 4 * V * sizeof(double), G->stream);
     }
     if (ext.l2_persist && !replay) {
         cudaStreamAttrValue attr{};
@@ -1548,7 +1586,7 @@ int pgl_graph_layout(pgl_graph* g, const pgl_layout_config* cfg, const pgl_layou
                      pgl_run_stats* stats) {
     return guarded([&] {
         if (!g) raise(PGL_ERR_INVALID_PARAMETER, "graph is null");
-        graph_layout(g, cfg, ext, reuse, cb, cb_wants_coords, user, out_coords, stats);
+        graph_layout(g, cfg, ext, reuse, cb, cb_wants_coords, user, out_coords, stats, nullptr);
     });
 }
 
@@ -1574,8 +1612,23 @@ int pgl_layout_run(int device, const pgl_graph_view* v, const pgl_layout_config*
         const ViewSummary s = summarize(v);
         if (v->n_paths == 0 || !s.usable)
             raise(PGL_ERR_DEGENERATE_GRAPH, "layout needs at least one path with two or more steps");
-        std::unique_ptr<pgl_graph> G(create_graph(device, v));
-        graph_layout(G.get(), cfg, ext, reuse, cb, cb_wants_coords, user, out_coords, stats);
+        // init_layout (host, sequential RNG, bit-exact) runs on its own
+        // thread while the graph is packed and uploaded; it needs only the
+        // node lengths and the seed
+        PinnedBuf init;
+        init.alloc(std::max<uint64_t>(4 * v->n_nodes, 1) * sizeof(double));
+        std::thread init_thread(
+            [&] { init_layout(v, s.total_nt, cfg->global_seed, static_cast<double*>(init.p)); });
+        std::unique_ptr<pgl_graph> G;
+        try {
+            G.reset(create_graph(device, v));
+        } catch (...) {
+            init_thread.join();
+            throw;
+        }
+        init_thread.join();
+        graph_layout(G.get(), cfg, ext, reuse, cb, cb_wants_coords, user, out_coords, stats,
+                     static_cast<const double*>(init.p));
         DeviceGuard dg(device);
         G.reset();
     });
@@ -1863,7 +1916,7 @@ int pgl_layout_shards(int n_devices, const int* devices, int n_graphs, const pgl
                         const double t0 = now_s();
                         std::unique_ptr<pgl_graph> G(create_graph(devices[d], graphs[k]));
                         graph_layout(G.get(), &cfgs[k], ext, 0, nullptr, 0, nullptr,
-                                     out_coords ? out_coords[k] : nullptr, stats ? &stats[k] : nullptr);
+                                     out_coords ? out_coords[k] : nullptr, stats ? &stats[k] : nullptr, nullptr);
                         {
                             DeviceGuard dg(devices[d]);
                             G.reset();
