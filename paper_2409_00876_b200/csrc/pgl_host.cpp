@@ -526,7 +526,7 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
     dlen.alloc(std::max<uint64_t>(V, 1));
     dsteps.alloc(S);
     PGL_CUDA(copy_async(dlen.p, len32.data(), V * sizeof(uint32_t), cudaMemcpyHostToDevice, G->stream));
-    const uint64_t kChunk = std::min<uint64_t>(1ULL << 23, S);  // <= 8 Mi steps = 32 MiB
+    const uint64_t kChunk = std::min<uint64_t>(1ULL << 25, S);  // <= 32 Mi steps = 128 MiB
     G->pin.alloc(2 * kChunk * sizeof(uint32_t));
     uint32_t* bufs[2] = {static_cast<uint32_t*>(G->pin.p), static_cast<uint32_t*>(G->pin.p) + kChunk};
     cudaEvent_t done[2];
