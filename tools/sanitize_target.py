@@ -17,12 +17,18 @@ with P.DeviceGraph(g) as dg:
                 P.LayoutExt(kernel_variant=8, coord_precision=P.COORD_F32_ANCHORED),
                 P.LayoutExt(kernel_variant=7, unit_order=P.ORDER_RANDOM),
                 P.LayoutExt(kernel_variant=6, coord_precision=P.COORD_F32_ANCHORED),
-                P.LayoutExt(sampling=P.SAMPLING_IID)]:
+                P.LayoutExt(kernel_variant=10, coord_precision=P.COORD_F32_ANCHORED),
+                P.LayoutExt(sampling=P.SAMPLING_IID),
+                P.LayoutExt(sampling=P.SAMPLING_IID, kernel_variant=4, coord_precision=P.COORD_F32_ANCHORED),
+                P.LayoutExt(sampling=P.SAMPLING_IID, kernel_variant=7),
+                P.LayoutExt(sampling=P.SAMPLING_IID, kernel_variant=5)]:
         outs.append(dg.layout(cfg, ext=ext))
     outs.append(dg.layout(P.LayoutConfig(n_iters=1, global_seed=5), ext=P.LayoutExt(mode=P.MODE_REPLAY)))
     dg.stress(7, 5)
     dg.stress(7, 2, method=P.SPS_STREAM)
 small = P.generate_synthetic_pangenome(3, 300, 3, 0.05)
+outs.append(P.run_layout(small, P.LayoutConfig(n_iters=3, batch_size=7, threads=4),
+                         ext=P.LayoutExt(sampling=P.SAMPLING_IID, kernel_variant=4)))
 outs.append(P.run_layout_reuse(small, P.LayoutConfig(n_iters=3, drf=2, srf=2), ext=P.LayoutExt(reuse_shuffle=1)))
 P.exact_path_stress(small, outs[-1])
 assert all(np.isfinite(o).all() for o in outs)
