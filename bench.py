@@ -218,7 +218,7 @@ def hbm_peak():
 def kernel_name(variant: int) -> str:
     """The SGD kernel a layout ran (pgl_timing.kernel_variant: 0 = the
     i.i.d. kernel, 7-12 the lean tile kernel, else the general tile kernel)."""
-    return "k_sgd_hogwild" if variant == 0 else ("k_sgd_lean" if 7 <= variant <= 12 else "k_sgd_tiles")
+    return "k_sgd_hogwild" if variant == 0 else ("k_sgd_lean" if 7 <= variant <= 14 else "k_sgd_tiles")
 
 
 def ncu_key(config: str, coord: str, variant: int) -> str:
@@ -504,6 +504,9 @@ def run_ours(args, dist: Dist):
 
     peak, peak_src = hbm_peak()
     payload = BYTES_PER_UPDATE[args.coord]
+    rec8 = timing.variant in (13, 14)  # 8-byte records: the primary's 8 B + the partner's two (k, k+1)
+    if rec8:
+        payload -= 32 - 24
     per_launch = (10 * S // cfg.srf) * cfg.drf
     payload_gbs = per_launch * payload / (sgd_launch_ms / 1e3) / 1e9
     traffic, ncu_ms, ncu_cache = ncu_traffic(args.config, args.coord, timing.variant)
@@ -538,7 +541,8 @@ def run_ours(args, dist: Dist):
                          "model": model, "launch_ms": sgd_launch_ms, "ncu_launch_ms": ncu_ms,
                          "payload": {"bytes_per_update": payload, "achieved": payload_gbs,
                                      "frac": payload_gbs / peak,
-                                     "model": "2 step records + 2 endpoint reads + 2 endpoint writes"},
+                                     "model": ("8-byte primary record + 2 partner records (k, k+1)" if rec8 else
+                                               "2 step records") + " + 2 endpoint reads + 2 endpoint writes"},
                          "peak_source": peak_src, "ncu": ncu_cache},
             "iid_sampler": iid,
             "c4": c4,

@@ -384,6 +384,7 @@ struct pgl_graph {
     std::vector<uint64_t> node_len;      // host copy (init_layout)
     std::vector<uint64_t> path_n_steps;  // host copy (zipf supports)
     DevBuf<StepRec> step;
+    DevBuf<uint2> rec8;                  // 8-byte records, built on first use (lean variants 13/14)
     DevBuf<uint64_t> cum;
     DevBuf<uint32_t> guide;
     DevBuf<uint32_t> sguide;
@@ -406,6 +407,7 @@ struct pgl_graph {
     void set_stream(cudaStream_t st) {
         stream = st;
         step.s = cum.s = stream;
+        rec8.s = stream;
         guide.s = sguide.s = stream;
         pc.s = fguide.s = stream;
         zalias.s = stream;
@@ -419,6 +421,7 @@ struct pgl_graph {
         if (sps.cnt) cudaFree(sps.cnt);
         if (sps.scal) cudaFree(sps.scal);
         step.release();
+        rec8.release();
         cum.release();
         guide.release();
         sguide.release();
@@ -438,6 +441,7 @@ struct pgl_graph {
     DevGraph dev() const {
         DevGraph d;
         d.step = step.p;
+        d.rec8 = rec8.p;
         d.cum = cum.p;
         d.guide = guide.p;
         d.pc = pc.p;
@@ -731,16 +735,18 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
         // synchronous apply at 4 CTAs/SM (variant 10: C3 58.0 vs 53.6 G upd/s
         // for the staged variant 7, profiles/r02_ab_sync_early.jsonl);
         // the register pipeline's shorter read-to-write window where the
-        // cap binds hard (config 1)
-        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 10 : 6) : 1;
+        // cap binds hard (config 1). The lean default reads the 8-byte
+        // records (variant 13: C3 61.2 vs 58.6, C2 63.9 vs 59.9 G upd/s for
+        // variant 10, profiles/r02_ab_rec8_c{3,2}.jsonl)
+        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 13 : 6) : 1;
     }
-    if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 12))
-        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-12");
-    if (v >= 7 && v <= 12 && (!lean_ok || force64))
+    if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 14))
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-14");
+    if (v >= 7 && v <= 14 && (!lean_ok || force64))
         raise(PGL_ERR_INVALID_PARAMETER,
-              "pgl_layout_ext.kernel_variant 7-12 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
+              "pgl_layout_ext.kernel_variant 7-14 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
               "pair_window 1 or 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
-    return v | force64 | (v >= 7 && v <= 12 && ext.diag ? 32 : 0);
+    return v | force64 | (v >= 7 && v <= 14 && ext.diag ? 32 : 0);
 }
 
 // The i.i.d. kernel's variant when pgl_layout_ext.kernel_variant is 0
@@ -1012,7 +1018,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         if (ext.unit_order == PGL_ORDER_RANDOM &&
-            (ext.sampling != PGL_SAMPLING_TILES || (shape.variant & 15) < 7 || (shape.variant & 15) > 12))
+            (ext.sampling != PGL_SAMPLING_TILES || (shape.variant & 15) < 7 || (shape.variant & 15) > 14))
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the random order needs the lean tile kernel "
                                              "(kernel_variant 7 or 8)");
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -1052,6 +1058,11 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     cudaDeviceGetLimit(&prev_gran, cudaLimitMaxL2FetchGranularity);
     if (!replay) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, ext.l2_fetch_bytes ? ext.l2_fetch_bytes : 32);
     const uint64_t spi = 10 * G->sum.total_steps / cfg.srf;  // engine.cpp:197
+    if (!replay && ext.sampling == PGL_SAMPLING_TILES && ((shape.variant & 15) == 13 || (shape.variant & 15) == 14) &&
+        !G->rec8.p) {
+        G->rec8.alloc(G->sum.total_steps + G->n_paths);
+        build_rec8_device(G->step.p, G->cum.p, G->n_paths, G->sum.total_steps, G->rec8.p, G->stream);
+    }
     const DevGraph dg_ = G->dev();
     // sampler diagnostics of the Hogwild kernels (pgl_layout_diag)
     DevBuf<unsigned int> visits;
@@ -1088,7 +1099,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         a.n_warps = n_warps;
         a.units = (spi + 31) / 32;
         const bool lean = !replay && ext.sampling == PGL_SAMPLING_TILES &&
-                          ((shape.variant & 15) >= 7 && (shape.variant & 15) <= 12);
+                          ((shape.variant & 15) >= 7 && (shape.variant & 15) <= 14);
         a.units_full = spi / 32;
         a.tail_n = static_cast<uint32_t>(spi % 32);
         {   // unit order of k_sgd_tiles: u = (a*k + b) mod U, gcd(a, U) = 1,

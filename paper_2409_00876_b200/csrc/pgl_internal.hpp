@@ -94,6 +94,11 @@ struct DevGraph {
     const uint32_t* sguide;   // [1 << sguide_bits] path of step (b << sguide_shift)
     uint32_t sguide_shift;
     uint32_t sguide_bits;
+    // [S + P] 8-byte step records {node | reverse << 31, offset} with one
+    // sentinel {0, total_len} after each path, so step k's two endpoint
+    // positions are offset(k) and offset(k + 1) (lean variants 13/14; built
+    // on first use, paths < 2^32 nt)
+    const uint2* rec8;
 };
 
 struct IterArgs {
@@ -241,6 +246,8 @@ void launch_anch_to_f64(const void* src, double* dst, uint64_t n_nodes, void* st
 void launch_reanchor(void* store, uint64_t n_nodes, void* stream);
 // out[0] = blocks of 32 node ids whose path positions span more than
 // max_span_256nt * 256 nt, out[1] = blocks visited by some step
+void build_rec8_device(const StepRec* step, const uint64_t* cum, uint32_t P, uint64_t S, uint2* out,
+                       cudaStream_t stream);
 void block_span_stats(const StepRec* step, uint64_t S, uint64_t n_nodes, uint32_t max_span_256nt,
                       unsigned long long* out, void* stream);
 void launch_count_nonfinite(const void* coords, int coord_kind, uint64_t n_nodes, unsigned long long* out,

@@ -62,7 +62,34 @@ __global__ void k_build_records(const uint32_t* __restrict__ steps, const uint32
     }
 }
 
+// 8-byte records (DevGraph::rec8): step gi of path p goes to gi + p; the
+// path's sentinel after its last step carries the far end position. For a
+// forward step pos_start = offset < pos_end, for a reverse one the other
+// way round (path_position, graph.hpp:98-109), so the orientation is
+// pos_start > pos_end and the step's offset is the smaller of the two.
+__global__ void k_build_rec8(const StepRec* __restrict__ step, const uint64_t* __restrict__ cum, uint32_t P,
+                             uint64_t S, uint2* __restrict__ out) {
+    for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; gi < S;
+         gi += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t lo = 0, hi = P;  // largest p with cum[p] <= gi
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (cum[mid] <= gi) lo = mid; else hi = mid;
+        }
+        const StepRec r = step[gi];
+        const bool rev = r.ps_lo > r.pe_lo;
+        out[gi + lo] = make_uint2(r.node | (rev ? 0x80000000u : 0u), rev ? r.pe_lo : r.ps_lo);
+        if (gi + 1 == cum[lo + 1]) out[gi + lo + 1] = make_uint2(0u, rev ? r.ps_lo : r.pe_lo);
+    }
+}
+
 }  // namespace
+
+void build_rec8_device(const StepRec* step, const uint64_t* cum, uint32_t P, uint64_t S, uint2* out,
+                       cudaStream_t stream) {
+    k_build_rec8<<<148 * 16, 256, 0, stream>>>(step, cum, P, S, out);
+    PGL_CUDA(cudaGetLastError());
+}
 
 void build_records_device(const uint32_t* d_steps, const uint32_t* d_node_len, const uint64_t* d_cum, uint32_t P,
                           uint64_t S, StepRec* d_out, void* stream_) {

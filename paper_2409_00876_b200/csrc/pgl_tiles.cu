@@ -703,7 +703,11 @@ __host__ __device__ constexpr size_t lean_smem_bytes(bool anchored) {
 // kSync 2 (variants 11, 12): the same loads issued at the start of the
 // round and consumed after the round's resolve and select, which hide their
 // latency (window: one round's integer work, no shared-memory staging).
-template <typename T, int kMinBlocks, bool kDiag, int kSync = 0>
+// kRec8 (variants 13/14, synchronous apply): the records come from the
+// 8-byte array DevGraph::rec8 -- a lane copies records k and k+1 of its path
+// (offset(k+1) is the far end of step k) into its 16-byte slot, so a unit's
+// primary records are 264 contiguous bytes instead of 512.
+template <typename T, int kMinBlocks, bool kDiag, int kSync = 0, bool kRec8 = false>
 __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* __restrict__ coords, DevRng rng,
                                                                DevStats* stats, IterArgs a) {
     const uint32_t tid = blockIdx.x * 256u + threadIdx.x;
@@ -806,7 +810,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         uint32_t p = 0, pbase = 0, n = 0, zn = 0;
         uint64_t zt = 0;
         bool zdef = false;
-        if (active) p = path_of_step_fat<uint32_t>(g, a, gi, cooling, pbase, n, zn, zt, zdef);
+        // (kRec8: inactive lanes of the partial unit too -- their slot must
+        // hold their own step's records for in-unit partners)
+        if (active || kRec8) p = path_of_step_fat<uint32_t>(g, a, gi, cooling, pbase, n, zn, zt, zdef);
         bool shared = false;
         uint32_t tag = 0;
         if (pw_shared) {  // tag: bits 0-28 path, 30 draw valid, 31 hop sign
@@ -830,6 +836,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
                 if (lane == 0) mbar_arrive(bar);
             }
+        } else if constexpr (kRec8) {
+            const uint2* src = g.rec8 + gi + p;
+            cp_async<8>(reinterpret_cast<char*>(dst_i + lane), src, pol_stream);
+            cp_async<8>(reinterpret_cast<char*>(dst_i + lane) + 8, src + 1, pol_stream);
         } else {
             cp_async<16>(dst_i + lane, g.step + gi, pol_stream);
         }
@@ -869,6 +879,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
         fl |= 1u | ((coins & 4u) ? 0u : 2u) | ((coins & 8u) ? 0u : 4u);
         if (gj - i0 < ul) {  // in-unit (unsigned: gj >= i0); a wrapped unit's low part copies its own
             fl |= 8u | ((gbase + gj - i0) << 8);
+        } else if constexpr (kRec8) {
+            const uint2* src = g.rec8 + gj + p;
+            cp_async<8>(reinterpret_cast<char*>(dst_j + lane), src, pol_stream);
+            cp_async<8>(reinterpret_cast<char*>(dst_j + lane) + 8, src + 1, pol_stream);
         } else {
             cp_async<16>(dst_j + lane, g.step + gj, pol_stream);
         }
@@ -944,8 +958,18 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_sgd_lean(DevGraph g, void* 
                 // 1 shared-memory wavefront each instead of 4 for the record
                 const uint32_t* wi = &s_ri[prv][wib][lane].node;
                 const uint32_t* wj = (fs & 8u) ? &s_ri[prv][wib][(fs >> 8) & 31].node : &s_rj[prv][wib][lane].node;
-                const uint32_t ni = wi[0], nj = wj[0];
-                const uint32_t pi = wi[(fs & 2u) ? 2 : 1], pj = wj[(fs & 4u) ? 2 : 1];  // pe_lo : ps_lo
+                uint32_t ni, nj, pi, pj;
+                if constexpr (kRec8) {  // {node | rev << 31, offset(k)}, {next node, offset(k + 1)}
+                    ni = wi[0] & 0x7FFFFFFFu;
+                    nj = wj[0] & 0x7FFFFFFFu;
+                    pi = (((fs >> 1) ^ (wi[0] >> 31)) & 1u) ? wi[3] : wi[1];  // end xor reverse: offset(k + 1)
+                    pj = (((fs >> 2) ^ (wj[0] >> 31)) & 1u) ? wj[3] : wj[1];
+                } else {
+                    ni = wi[0];
+                    nj = wj[0];
+                    pi = wi[(fs & 2u) ? 2 : 1];  // pe_lo : ps_lo
+                    pj = wj[(fs & 4u) ? 2 : 1];
+                }
                 res = LeanRes{ni, nj, fs, pi > pj ? pi - pj : pj - pi};
                 if (kSync == 1 && PGL_LEAN_SYNC_PREFETCH && res.dref) {
                     // synchronous apply next round: pull the endpoints' lines
@@ -1056,6 +1080,10 @@ const void* tiles_fn_t(int variant) {
         if (variant == 11 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, 2>);
         if (variant == 12) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false, 2>);
         if (variant == 12 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, 2>);
+        if (variant == 13) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, false, 1, true>);
+        if (variant == 13 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, 1, true>);
+        if (variant == 14) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, 1, true>);
+        if (variant == 14 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, 1, true>);
     }
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
@@ -1071,7 +1099,7 @@ const void* tiles_fn(int variant, bool k32) {
 size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
-    if (variant >= 7 && variant <= 12)
+    if (variant >= 7 && variant <= 14)
         return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0) +
                (PGL_LEAN_BULK ? 8 * 2 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots

@@ -760,7 +760,7 @@ def test_production_kernel_sps_parity_mid(pgl, ref, gpu, prec):
         for seed in gold["layout"]["seeds"]:
             lay = dg.layout(pgl.LayoutConfig(global_seed=seed), ext=ext)
             tm = dg.timing()
-            assert 7 <= tm.variant <= 12, tm.variant  # the production (lean) kernel ran
+            assert 7 <= tm.variant <= 14, tm.variant  # the production (lean) kernel ran
             got.append(ref.sps(gr, lay, gold["metric"]["seed"], gold["metric"]["spn"]).mean)
     ratio = np.median(got) / gold["median_sps"]
     assert 0.98 <= ratio <= 1.02, (got, gold["median_sps"], ratio)

@@ -38,6 +38,8 @@ KERNELS = [
     pytest.param(0, 8, 2, id="tiles-v8-anch"),
     pytest.param(0, 9, 1, id="tiles-v9-f64"),
     pytest.param(0, 9, 2, id="tiles-v9-anch"),
+    pytest.param(0, 13, 1, id="tiles-v13-f64"),
+    pytest.param(0, 13, 2, id="tiles-v13-anch"),
     pytest.param(1, 0, 1, id="iid-f64"),
     pytest.param(1, 0, 2, id="iid-anch"),
     pytest.param(1, 2, 1, id="iid-d3-f64"),
@@ -75,7 +77,7 @@ def test_device_accounting_config1(pgl, gpu, samp, variant, prec):
 @pytest.mark.parametrize("samp,variant,prec", KERNELS)
 @pytest.mark.parametrize("drf,srf", [(2, 2), (4, 4), (2, 3), (4, 1)])
 def test_device_accounting_reuse(pgl, gpu, samp, variant, prec, drf, srf):
-    if variant in (7, 8, 9):
+    if samp == 0 and 7 <= variant <= 14:
         pytest.skip("the lean kernel covers drf 1 only (the host picks variant 6 for reuse runs)")
     g = pgl.generate_synthetic_pangenome(3, 400, 3, 0.05)
     st = pgl.RunStats()
@@ -115,7 +117,7 @@ def test_device_accounting_invalid_selections(pgl, gpu):
 
 # ---- primary visits ----------------------------------------------------------------
 
-@pytest.mark.parametrize("variant", [1, 6, 8])
+@pytest.mark.parametrize("variant", [1, 6, 8, 13])
 @pytest.mark.parametrize("srf", [1, 3, 4, 7])
 def test_tile_visits_rotate(pgl, gpu, variant, srf):
     """The tile sampler's enumeration: in every iteration each step is the
@@ -173,7 +175,7 @@ def zipf_pmf(n, theta):
 
 SAMPLER_KERNELS = [pytest.param(0, 1, id="tiles-v1"), pytest.param(0, 6, id="tiles-v6"),
                    pytest.param(0, 7, id="tiles-v7"), pytest.param(0, 8, id="tiles-v8"),
-                   pytest.param(0, 9, id="tiles-v9"),
+                   pytest.param(0, 9, id="tiles-v9"), pytest.param(0, 13, id="tiles-v13"),
                    pytest.param(1, 0, id="iid")]
 
 
@@ -258,7 +260,7 @@ def test_outcome_frequencies_two_step_path(pgl, gpu, samp, variant):
     1/4 of its draws (two collisions on a two-step path). So P(applied) =
     9/16 for uniform selections and 3/4 for cooling ones, +-0.02. (The lean
     kernels need >= 32 steps: 64 disjoint two-step paths, same frequencies.)"""
-    n_paths, n_iters = (64, 200) if variant in (7, 8, 9) else (1, 8000)
+    n_paths, n_iters = (64, 200) if samp == 0 and 7 <= variant <= 14 else (1, 8000)
     g = pgl.build_graph([5] * (2 * n_paths), [[(2 * p, 0), (2 * p + 1, 0)] for p in range(n_paths)])
     d = pgl.LayoutDiag()
     pgl.run_layout(g, pgl.LayoutConfig(n_iters=n_iters, global_seed=9),
@@ -294,7 +296,7 @@ def test_lean_kernel_preconditions(pgl, gpu):
             pgl.run_layout(g, pgl.LayoutConfig(n_iters=2), ext=pgl.LayoutExt(**ext))
 
 
-@pytest.mark.parametrize("variant", [7, 9])
+@pytest.mark.parametrize("variant", [7, 9, 13])
 @pytest.mark.parametrize("unit_len", [1, 4, 32])
 def test_lean_random_units_visit_uniformly(pgl, gpu, variant, unit_len):
     """PGL_ORDER_RANDOM with unit_len picks: every step's primary-visit count
@@ -318,7 +320,7 @@ def test_lean_random_units_visit_uniformly(pgl, gpu, variant, unit_len):
     assert sst.chi2.sf(chi2, 15) > 1e-4, chi2
 
 
-@pytest.mark.parametrize("variant", [7, 8])
+@pytest.mark.parametrize("variant", [7, 8, 13, 14])
 @pytest.mark.parametrize("prec", [0, 1, 2])
 def test_lean_kernel_batches_and_tail(pgl, gpu, variant, prec):
     """Every unit is one batch of 32 picks opened by lane 0, the partial last
@@ -339,3 +341,23 @@ def test_lean_kernel_batches_and_tail(pgl, gpu, variant, prec):
     assert abs(frac - 0.5) < 5 / np.sqrt(st.batches_first_half), frac
     assert st.primary_steps == st.updates_attempted == 30 * N
     assert st.updates_applied + st.updates_skipped == st.updates_attempted
+
+
+@pytest.mark.parametrize("base,rec8", [(10, 13), (9, 14)])
+@pytest.mark.parametrize("prec", [1, 2])
+def test_lean_rec8_matches_16_byte_records(pgl, gpu, base, rec8, prec):
+    """Variants 13/14 read 8-byte records {node | reverse << 31, offset}
+    (offset(k+1) = the far end of step k, a sentinel after each path)
+    instead of the 16-byte records; with one warp the kernel is
+    deterministic, so on a nested graph (reverse steps, revisits, path ends
+    inside units) both record formats must give the identical layout and
+    RunStats."""
+    g = pgl.generate_nested_pangenome(7, 600, 12, 3, 0.05)
+    outs, stats = [], []
+    for v in (base, rec8):
+        st = pgl.RunStats()
+        outs.append(pgl.run_layout(g, pgl.LayoutConfig(n_iters=6, global_seed=11), stats=st,
+                                   ext=pgl.LayoutExt(kernel_variant=v, coord_precision=prec, max_warps=1)))
+        stats.append((st.primary_steps, st.updates_applied, st.updates_skipped))
+    assert stats[0] == stats[1]
+    assert np.array_equal(outs[0], outs[1])
