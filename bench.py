@@ -218,7 +218,7 @@ def hbm_peak():
 def kernel_name(variant: int) -> str:
     """The SGD kernel a layout ran (pgl_timing.kernel_variant: 0 = the
     i.i.d. kernel, 7-12 the lean tile kernel, else the general tile kernel)."""
-    return "k_sgd_hogwild" if variant == 0 else ("k_sgd_lean" if 7 <= variant <= 15 else "k_sgd_tiles")
+    return "k_sgd_hogwild" if variant == 0 else ("k_sgd_lean" if 7 <= variant <= 14 else "k_sgd_tiles")
 
 
 def ncu_key(config: str, coord: str, variant: int) -> str:
@@ -504,7 +504,7 @@ def run_ours(args, dist: Dist):
 
     peak, peak_src = hbm_peak()
     payload = BYTES_PER_UPDATE[args.coord]
-    rec8 = timing.variant in (13, 14, 15)  # 8-byte records: the primary's 8 B + the partner's two (k, k+1)
+    rec8 = timing.variant in (13, 14)  # 8-byte records: the primary's 8 B + the partner's two (k, k+1)
     if rec8:
         payload -= 32 - 24
     per_launch = (10 * S // cfg.srf) * cfg.drf

@@ -178,12 +178,11 @@ typedef struct pgl_layout_ext {
     uint32_t max_warps;       /* 0 = auto concurrency cap (scales with node count) */
     uint32_t block_threads;   /* 0 = default (256) */
     uint32_t l2_persist;      /* 1 = L2 persistence window on the coordinate array */
-    uint32_t kernel_variant;  /* tile kernel: 0 = auto (13 for LayoutConfig{}-shaped runs once
+    uint32_t kernel_variant;  /* tile kernel: 0 = auto (10 for LayoutConfig{}-shaped runs once
                                  the concurrency cap allows full residency, 6 for the general
                                  case, 1 where the cap binds); 1/2 = register pipeline, 2/3
                                  CTAs/SM; 5/6 = cp.async pipeline via shared memory, 4/3
-                                 CTAs/SM; 7-14 = the lean kernel (pgl_tiles.cu; 13/14 read
-                                 8-byte step records).
+                                 CTAs/SM; 7-12 = the lean kernel (pgl_tiles.cu).
                                  i.i.d. kernel (PGL_SAMPLING_IID): 0 = auto; 8 = two-stage,
                                  2 CTAs/SM; 1-5: bit 0 = 3 CTAs/SM, variant >> 1 = rounds of
                                  step records in flight beyond the current one (depth 2-4);

@@ -740,13 +740,13 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
         // variant 10, profiles/r02_ab_rec8_c{3,2}.jsonl)
         v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 13 : 6) : 1;
     }
-    if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 15))
-        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-15");
-    if (v >= 7 && v <= 15 && (!lean_ok || force64))
+    if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 14))
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-14");
+    if (v >= 7 && v <= 14 && (!lean_ok || force64))
         raise(PGL_ERR_INVALID_PARAMETER,
-              "pgl_layout_ext.kernel_variant 7-15 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
+              "pgl_layout_ext.kernel_variant 7-14 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
               "pair_window 1 or 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
-    return v | force64 | (v >= 7 && v <= 15 && ext.diag ? 32 : 0);
+    return v | force64 | (v >= 7 && v <= 14 && ext.diag ? 32 : 0);
 }
 
 // The i.i.d. kernel's variant when pgl_layout_ext.kernel_variant is 0
@@ -1018,7 +1018,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         if (ext.unit_order == PGL_ORDER_RANDOM &&
-            (ext.sampling != PGL_SAMPLING_TILES || (shape.variant & 15) < 7 || (shape.variant & 15) > 15))
+            (ext.sampling != PGL_SAMPLING_TILES || (shape.variant & 15) < 7 || (shape.variant & 15) > 14))
             raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.unit_order: the random order needs the lean tile kernel "
                                              "(kernel_variant 7 or 8)");
         lanes = static_cast<uint64_t>(shape.blocks) * shape.threads;
@@ -1058,7 +1058,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
     cudaDeviceGetLimit(&prev_gran, cudaLimitMaxL2FetchGranularity);
     if (!replay) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, ext.l2_fetch_bytes ? ext.l2_fetch_bytes : 32);
     const uint64_t spi = 10 * G->sum.total_steps / cfg.srf;  // engine.cpp:197
-    if (!replay && ext.sampling == PGL_SAMPLING_TILES && ((shape.variant & 15) >= 13) &&
+    if (!replay && ext.sampling == PGL_SAMPLING_TILES && ((shape.variant & 15) == 13 || (shape.variant & 15) == 14) &&
         !G->rec8.p) {
         G->rec8.alloc(G->sum.total_steps + G->n_paths);
         build_rec8_device(G->step.p, G->cum.p, G->n_paths, G->sum.total_steps, G->rec8.p, G->stream);
@@ -1099,7 +1099,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
         a.n_warps = n_warps;
         a.units = (spi + 31) / 32;
         const bool lean = !replay && ext.sampling == PGL_SAMPLING_TILES &&
-                          ((shape.variant & 15) >= 7 && (shape.variant & 15) <= 15);
+                          ((shape.variant & 15) >= 7 && (shape.variant & 15) <= 14);
         a.units_full = spi / 32;
         a.tail_n = static_cast<uint32_t>(spi % 32);
         {   // unit order of k_sgd_tiles: u = (a*k + b) mod U, gcd(a, U) = 1,

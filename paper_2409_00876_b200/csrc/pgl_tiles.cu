@@ -1084,8 +1084,6 @@ const void* tiles_fn_t(int variant) {
         if (variant == 13 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 4, true, 1, true>);
         if (variant == 14) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, false, 1, true>);
         if (variant == 14 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 3, true, 1, true>);
-        if (variant == 15) return reinterpret_cast<const void*>(k_sgd_lean<T, 5, false, 1, true>);
-        if (variant == 15 + 32) return reinterpret_cast<const void*>(k_sgd_lean<T, 5, true, 1, true>);
     }
     return variant == 2   ? reinterpret_cast<const void*>(k_sgd_tiles<T, 3, 0, k32>)
            : variant == 5 ? reinterpret_cast<const void*>(k_sgd_tiles<T, 4, 1, k32>)
@@ -1101,7 +1099,7 @@ const void* tiles_fn(int variant, bool k32) {
 size_t tiles_smem(int variant, int coord_kind) {
     variant &= 15;
     const bool async = variant == 5 || variant == 6, anch = coord_kind == PGL_COORD_F32_ANCHORED;
-    if (variant >= 7 && variant <= 15)
+    if (variant >= 7 && variant <= 14)
         return lean_smem_bytes(anch) + (anch && PGL_LEAN_SMEM_RNG ? 256 * 4 * sizeof(uint64_t) : 0) +
                (PGL_LEAN_BULK ? 8 * 2 * sizeof(uint64_t) : 0);
     // anchored: + the generator state (4 u64 per thread) after the pipeline's slots
