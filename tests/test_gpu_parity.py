@@ -674,7 +674,13 @@ def test_index_from_view_offsets_when_not_prefix_sums(pgl, gpu):
     steps = [s.copy() for s in g.path_steps]
     steps[0]["offset"] = [0, 9, 12, 30]          # gaps: not the running sums
     odd = pgl.PangenomeGraph(g.node_len, steps)
-    for graph, arrs in ((g, g.path_steps), (odd, steps)):
+    # running-sum offsets, but a seq_len that is not the node's length (the
+    # compact upload's length fingerprint must reject it)
+    steps2 = [s.copy() for s in g.path_steps]
+    steps2[1]["seq_len"] = [4, 7]                  # node 3 has length 2
+    steps2[1]["offset"] = [0, 4]
+    odd2 = pgl.PangenomeGraph(g.node_len, steps2)
+    for graph, arrs in ((g, g.path_steps), (odd, steps), (odd2, steps2)):
         want = []
         for a in arrs:
             for st in a:
