@@ -736,7 +736,7 @@ constexpr uint32_t kHopLanes = 8;  // default lanes per shared Zipf hop
 // lean_ok: the run is one the lean async kernel (variants 7, 8) covers --
 // batch 32, drf 1, no warp-shuffle reuse, the shared window + Zipf-hop
 // sampler, 32 <= S < 2^30 steps, paths shorter than 2^32 nt.
-int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_ok) {
+int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_ok, bool rec8_ok) {
     int v = static_cast<int>(ext.kernel_variant & 15);
     const int force64 = static_cast<int>(ext.kernel_variant & 16);
     if (v == 0) {
@@ -751,7 +751,7 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
         // cap binds hard (config 1). The lean default reads the 8-byte
         // records (variant 13: C3 61.2 vs 58.6, C2 63.9 vs 59.9 G upd/s for
         // variant 10, profiles/r02_ab_rec8_c{3,2}.jsonl)
-        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? 13 : 6) : 1;
+        v = cap >= static_cast<uint32_t>(sms) * 8 ? (lean_ok && !force64 ? (rec8_ok ? 13 : 10) : 6) : 1;
     }
     if (v != 1 && v != 2 && v != 5 && v != 6 && !(v >= 7 && v <= 14))
         raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant: tile kernel variants are 0, 1, 2, 5-14");
@@ -759,6 +759,8 @@ int tile_variant(int device, const pgl_layout_ext& ext, uint32_t cap, bool lean_
         raise(PGL_ERR_INVALID_PARAMETER,
               "pgl_layout_ext.kernel_variant 7-14 (lean) needs batch_size 32, drf 1, no reuse_shuffle, "
               "pair_window 1 or 3, 32 <= steps < 2^30 and paths shorter than 2^32 nt");
+    if ((v == 13 || v == 14) && !rec8_ok)
+        raise(PGL_ERR_INVALID_PARAMETER, "pgl_layout_ext.kernel_variant 13/14 (8-byte records) needs fewer than 2^31 nodes");
     return v | force64 | (v >= 7 && v <= 14 && ext.diag ? 32 : 0);
 }
 
@@ -1027,7 +1029,7 @@ void graph_layout(pgl_graph* G, const pgl_layout_config* cfgp, const pgl_layout_
                     ? sgd_shape(G->device, kind, cap, static_cast<int>(ext.block_threads),
                                 ext.kernel_variant ? static_cast<int>(ext.kernel_variant) : kIidAutoVariant)
                     : tiles_shape(G->device, kind, cap, static_cast<int>(ext.block_threads),
-                                  tile_variant(G->device, ext, cap, lean_ok), G->sum.total_steps);
+                                  tile_variant(G->device, ext, cap, lean_ok, V < (1ULL << 31)), G->sum.total_steps);
         const uint64_t grid_warps = static_cast<uint64_t>(shape.blocks) * shape.threads / 32;
         n_warps = static_cast<uint32_t>(std::min<uint64_t>(grid_warps, cap));
         if (ext.unit_order == PGL_ORDER_RANDOM &&
