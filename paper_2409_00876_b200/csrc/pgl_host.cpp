@@ -515,9 +515,8 @@ void upload_tables(pgl_graph* G, const std::vector<uint64_t>& cum) {
 // the offsets and records exactly as for a GFA (build_records_device).
 // Valid when the view is what build_graph makes (graph.cpp:38-50): every
 // step's seq_len is its node's length and offsets are the running sums.
-// Checked while packing (offsets step by step, lengths by fingerprint);
-// returns false (nothing built) when a view is not of that form, and
-// pack_graph then uploads full records.
+// Checked step by step while packing; returns false (nothing built) when a
+// view is not of that form, and pack_graph then uploads full records.
 bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector<uint64_t>& cum) {
     const uint64_t S = G->sum.total_steps, V = v->n_nodes;
     if (V >= (1ULL << 31) || S == 0) return false;
@@ -538,11 +537,6 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
     PGL_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
     PGL_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
     std::atomic<int> bad_node{0}, irregular{0};
-    // seq_len == node_len[node] for every step is checked by fingerprint
-    // (step_len_mix: host over the streamed seq_len, device over node_len
-    // gathered from the uploaded node ids) instead of a random host read of
-    // node_len per step
-    std::atomic<uint64_t> fp_host{0};
     const uint64_t n_chunks = (S + kChunk - 1) / kChunk;
     for (uint64_t c = 0; c < n_chunks && !bad_node.load() && !irregular.load(); ++c) {
         uint32_t* buf = bufs[c & 1];
@@ -552,7 +546,6 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
             uint64_t k = k0 + b;
             uint32_t p = static_cast<uint32_t>(std::upper_bound(cum.begin(), cum.end(), k) - cum.begin() - 1);
             bool odd = false, bad = false;
-            uint64_t fp = 0;
             for (; k < k0 + e; ++k) {
                 while (k >= cum[p + 1]) ++p;
                 const pgl_path_step* ps = v->path_steps[p];
@@ -563,11 +556,9 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
                     break;
                 }
                 const uint64_t want = i ? ps[i - 1].offset + ps[i - 1].seq_len : 0;
-                odd |= st.offset != want || st.node_id >= (1u << 31);
-                fp += step_len_mix(k, st.seq_len);
+                odd |= st.seq_len != len32[st.node_id] || st.offset != want || st.node_id >= (1u << 31);
                 buf[k - k0] = st.node_id | (st.orient ? 1u << 31 : 0u);
             }
-            fp_host.fetch_add(fp, std::memory_order_relaxed);
             if (bad) bad_node.store(1, std::memory_order_relaxed);
             if (odd) irregular.store(1, std::memory_order_relaxed);
         });
@@ -580,10 +571,6 @@ bool pack_graph_compact(pgl_graph* G, const pgl_graph_view* v, const std::vector
     cudaEventDestroy(done[1]);
     if (bad_node.load()) raise(PGL_ERR_UNKNOWN_NODE, "path references a node outside the graph");
     if (irregular.load()) return false;
-    DevBuf<unsigned long long> scratch;
-    scratch.s = G->stream;
-    scratch.alloc(1);
-    if (step_len_fingerprint_device(dsteps.p, dlen.p, S, scratch.p, G->stream) != fp_host.load()) return false;
     build_records_device(dsteps.p, dlen.p, G->cum.p, G->n_paths, S, G->step.p, G->stream);
     PGL_CUDA(cudaStreamSynchronize(G->stream));
     return true;

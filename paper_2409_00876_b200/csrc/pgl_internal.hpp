@@ -246,22 +246,6 @@ void launch_anch_to_f64(const void* src, double* dst, uint64_t n_nodes, void* st
 void launch_reanchor(void* store, uint64_t n_nodes, void* stream);
 // out[0] = blocks of 32 node ids whose path positions span more than
 // max_span_256nt * 256 nt, out[1] = blocks visited by some step
-// Order-independent fingerprint of a step-length sequence: the sum over
-// steps k of mix(k, len(k)). The host sums it over the view's PathStep
-// seq_len while it streams the steps; the device over node_len[node(k)];
-// equal sums say (up to a 2^-64 chance) that every step's seq_len is its
-// node's length, without a random host read of node_len per step.
-#ifdef __CUDACC__
-__host__ __device__
-#endif
-inline uint64_t step_len_mix(uint64_t k, uint64_t len) {
-    uint64_t z = k * 0x9E3779B97F4A7C15ULL + len + 0x632BE59BD9B4E019ULL;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
-}
-uint64_t step_len_fingerprint_device(const uint32_t* d_steps, const uint32_t* d_node_len, uint64_t S,
-                                     unsigned long long* d_scratch, cudaStream_t stream);
 void build_rec8_device(const StepRec* step, const uint64_t* cum, uint32_t P, uint64_t S, uint2* out,
                        cudaStream_t stream);
 void block_span_stats(const StepRec* step, uint64_t S, uint64_t n_nodes, uint32_t max_span_256nt,

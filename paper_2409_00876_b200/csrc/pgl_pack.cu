@@ -83,28 +83,7 @@ __global__ void k_build_rec8(const StepRec* __restrict__ step, const uint64_t* _
     }
 }
 
-__global__ void k_step_len_fingerprint(const uint32_t* __restrict__ steps, const uint32_t* __restrict__ node_len,
-                                       uint64_t S, unsigned long long* __restrict__ out) {
-    uint64_t acc = 0;
-    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < S;
-         k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        acc += step_len_mix(k, node_len[steps[k] & 0x7FFFFFFFu]);
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(acc));
-}
-
 }  // namespace
-
-uint64_t step_len_fingerprint_device(const uint32_t* d_steps, const uint32_t* d_node_len, uint64_t S,
-                                     unsigned long long* d_scratch, cudaStream_t stream) {
-    PGL_CUDA(cudaMemsetAsync(d_scratch, 0, sizeof(unsigned long long), stream));
-    k_step_len_fingerprint<<<148 * 8, 256, 0, stream>>>(d_steps, d_node_len, S, d_scratch);
-    PGL_CUDA(cudaGetLastError());
-    unsigned long long h = 0;
-    PGL_CUDA(copy_async(&h, d_scratch, sizeof h, cudaMemcpyDeviceToHost, stream));
-    PGL_CUDA(cudaStreamSynchronize(stream));
-    return h;
-}
 
 void build_rec8_device(const StepRec* step, const uint64_t* cum, uint32_t P, uint64_t S, uint2* out,
                        cudaStream_t stream) {
